@@ -1,0 +1,339 @@
+// eb_brute.cu -- K4: brute-force subset search (reference
+// exhaustive_optimal(mode="subsets"), dftsp.py:288-313).
+//
+// The reference tries itertools.combinations(pool, z) for z = K..1 and
+// returns the first subset that passes check_direct.  Equivalently: the
+// largest z with any feasible subset, and within it the smallest
+// lexicographic rank; nodes_visited is then
+// sum_{z'>z} C(K,z') + rank + 1.  On the device every thread owns a chunk of
+// consecutive ranks of one level, unranks its first combination once, then
+// walks lexicographic successors keeping prefix sums per position, so each
+// subset costs O(positions changed) instead of O(z) -- while every sum is
+// still the left-to-right fold check_direct computes (prefix sums of the same
+// sequence ARE the same fold).  A block-level (batch kernel) or grid-level
+// (range kernel) atomicMin keeps the first feasible rank.
+#include <climits>
+
+#include "eb_internal.cuh"
+
+namespace eb {
+
+__device__ uint64_t g_binom[EB_MAX_K + 1][EB_MAX_K + 1];
+
+namespace {
+
+__global__ void binom_init_kernel() {
+  int n = threadIdx.x;
+  if (n > EB_MAX_K) return;
+  // row n: C(n, k) -- computed sequentially by one thread per row (exact).
+  uint64_t c = 1;
+  for (int k = 0; k <= EB_MAX_K; ++k) {
+    if (k > n) { g_binom[n][k] = 0; continue; }
+    g_binom[n][k] = c;
+    // C(n, k+1) = C(n, k) * (n - k) / (k + 1), exact in 128-bit
+    unsigned __int128 t = (unsigned __int128)c * (unsigned)(n - k);
+    c = (uint64_t)(t / (unsigned)(k + 1));
+  }
+}
+
+__device__ __forceinline__ uint64_t binom(int n, int k) {
+  if (k < 0 || n < 0 || k > n) return 0;
+  return g_binom[n][k];
+}
+
+// Per-instance member terms, in pool order (check_direct's summation order).
+struct Members {
+  double a[EB_MAX_K];      // float(s) * k_up       feasibility.py:204
+  double b[EB_MAX_K];      // float(n) * k_down     feasibility.py:205
+  double ws[EB_MAX_K];     // waiting + slots       feasibility.py:222
+  double dl[EB_MAX_K];     // deadline
+  int64_t far[EB_MAX_K];   // flops_autoregressive(padded, n)
+  int32_t nout[EB_MAX_K];
+  int n;
+  int status;              // link-math error (raised inside check_direct)
+  int64_t m1, kvp, kv, fi; // weight bytes, kv*padded, kv, flops_initial(padded)
+  double alpha, M, beta, C, cap_s;
+  int has_cap;
+};
+
+// Cooperative (block) load of one instance's members; returns after sync.
+__device__ void load_members(Members& S, const Ctx& c, const eb_requests& req, int64_t r0, int n) {
+  __shared__ int s_pad;
+  __shared__ int s_err;
+  if (threadIdx.x == 0) { s_pad = 0; s_err = INT_MAX; }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicMax(&s_pad, req.prompt_tokens[r0 + i]);
+  __syncthreads();
+  const int padded = s_pad;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int64_t r = r0 + i;
+    double ku = 0.0, kd = 0.0;
+    int st = k_up_of(c, req.channel_gain[r], req.uplink_power_w[r], &ku);
+    if (!st) st = k_dn_of(c, req.channel_gain[r], &kd);
+    if (st) atomicMin(&s_err, i * 64 + st);
+    int s = req.prompt_tokens[r], no = req.output_tokens[r];
+    S.a[i] = mul(i2d(s), ku);
+    S.b[i] = mul(i2d(no), kd);
+    S.ws[i] = add(req.waiting_s[r], c.slots);
+    S.dl[i] = req.deadline_s[r];
+    S.far[i] = flops_autoregressive(c.m, padded, no);
+    S.nout[i] = no;
+  }
+  if (threadIdx.x == 0) {
+    S.n = n;
+    S.m1 = weight_bytes(c.m);
+    S.kv = kv_per_token(c.m);
+    S.kvp = S.kv * (int64_t)padded;
+    S.fi = flops_initial(c.m, padded);
+    S.alpha = c.alpha; S.M = c.M; S.beta = c.beta; S.C = c.C; S.cap_s = c.cap_s;
+    S.has_cap = c.has_cap;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) S.status = (s_err == INT_MAX) ? 0 : (s_err & 63);
+  __syncthreads();
+}
+
+// check_direct on the current combination given its prefix folds.
+__device__ __forceinline__ bool feasible(const Members& S, int z, const uint8_t* idx,
+                                         double up, double dn, int64_t sn, int64_t sf) {
+  if (!(leq(up, 1.0) && leq(dn, 1.0))) return false;
+  int64_t mem = S.m1 + S.kvp * z;
+  mem += S.kv * sn;
+  if (!leq(mul(S.alpha, i2d(mem)), S.M)) return false;
+  int64_t flops = (int64_t)z * S.fi + sf;
+  double cs = div(mul(S.beta, i2d(flops)), S.C);
+  if (S.has_cap && !leq(cs, S.cap_s)) return false;
+  for (int j = 0; j < z; ++j)
+    if (!leq(add(S.ws[idx[j]], cs), S.dl[idx[j]])) return false;
+  return true;
+}
+
+// Scan ranks [r_lo, r_hi) of level z (lex order) and return the first
+// feasible rank, or -1.  `stop` is polled so a thread quits once an earlier
+// rank is known feasible.
+__device__ int64_t scan_chunk(const Members& S, int z, int64_t r_lo, int64_t r_hi,
+                              const unsigned long long* stop) {
+  const int n = S.n;
+  uint8_t idx[EB_MAX_K];
+  double pu[EB_MAX_K + 1], pd[EB_MAX_K + 1];
+  int64_t ps[EB_MAX_K + 1], pf[EB_MAX_K + 1];
+  // unrank r_lo
+  {
+    uint64_t r = (uint64_t)r_lo;
+    int v = 0;
+    for (int j = 0; j < z; ++j) {
+      for (;;) {
+        uint64_t cnt = binom(n - v - 1, z - j - 1);
+        if (r < cnt) { idx[j] = (uint8_t)v; ++v; break; }
+        r -= cnt; ++v;
+      }
+    }
+  }
+  pu[0] = 0.0; pd[0] = 0.0; ps[0] = 0; pf[0] = 0;
+  int from = 0;
+  for (int64_t rank = r_lo; rank < r_hi; ++rank) {
+    for (int j = from; j < z; ++j) {
+      int i = idx[j];
+      pu[j + 1] = add(pu[j], S.a[i]);
+      pd[j + 1] = add(pd[j], S.b[i]);
+      ps[j + 1] = ps[j] + S.nout[i];
+      pf[j + 1] = pf[j] + S.far[i];
+    }
+    if (feasible(S, z, idx, pu[z], pd[z], ps[z], pf[z])) return rank;
+    if (((rank - r_lo) & 255) == 255 && *(volatile const unsigned long long*)stop < (unsigned long long)rank)
+      return -1;
+    // lexicographic successor (itertools.combinations order)
+    int j = z - 1;
+    while (j >= 0 && idx[j] == n - z + j) --j;
+    if (j < 0) break;
+    idx[j] += 1;
+    for (int q = j + 1; q < z; ++q) idx[q] = idx[q - 1] + 1;
+    from = j;
+  }
+  return -1;
+}
+
+struct BatchArgs {
+  const eb_context* ctxs;
+  int n_ctx;
+  int64_t n_inst;
+  const int64_t* offsets;
+  const int32_t* ctx_index;
+  int64_t req_base;
+  eb_requests req;
+  int cap;
+  int32_t* status;
+  int32_t* z_found;
+  int64_t* lexrank;
+  int64_t* nodes;
+  uint64_t* mask;
+};
+
+// One block per instance (many small instances).
+__global__ void __launch_bounds__(256) exh_batch_kernel(BatchArgs A) {
+  __shared__ Members S;
+  __shared__ unsigned long long best;
+  for (int64_t inst = blockIdx.x; inst < A.n_inst; inst += gridDim.x) {
+    int64_t row0 = A.offsets[inst];
+    int n = (int)(A.offsets[inst + 1] - row0);
+    int ci = A.ctx_index ? A.ctx_index[inst] : 0;
+    bool tid0 = threadIdx.x == 0;
+    if (n == 0 || n > A.cap || n > EB_MAX_K || ci < 0 || ci >= A.n_ctx) {
+      if (tid0) {
+        A.status[inst] = (ci < 0 || ci >= A.n_ctx) ? EB_ERR_INVALID_ARG
+                         : (n == 0) ? EB_OK
+                         : (n > A.cap) ? EB_ERR_CAP_EXCEEDED : EB_ERR_K_TOO_LARGE;
+        A.z_found[inst] = 0; A.lexrank[inst] = -1; A.nodes[inst] = 0;
+        if (A.mask) A.mask[inst] = 0;
+      }
+      __syncthreads();
+      continue;
+    }
+    const Ctx c = load_ctx(&A.ctxs[ci]);
+    load_members(S, c, A.req, row0 - A.req_base, n);
+    if (S.status) {
+      if (tid0) {
+        A.status[inst] = S.status; A.z_found[inst] = 0; A.lexrank[inst] = -1; A.nodes[inst] = 0;
+        if (A.mask) A.mask[inst] = 0;
+      }
+      __syncthreads();
+      continue;
+    }
+    int zf = 0;
+    int64_t rk = -1, skipped = 0;
+    for (int z = n; z >= 1; --z) {
+      uint64_t total = binom(n, z);
+      if (tid0) best = ULLONG_MAX;
+      __syncthreads();
+      uint64_t per = (total + blockDim.x - 1) / blockDim.x;
+      uint64_t lo = per * threadIdx.x;
+      uint64_t hi = lo + per < total ? lo + per : total;
+      if (lo < hi) {
+        int64_t r = scan_chunk(S, z, (int64_t)lo, (int64_t)hi, &best);
+        if (r >= 0) atomicMin(&best, (unsigned long long)r);
+      }
+      __syncthreads();
+      unsigned long long b = best;
+      __syncthreads();
+      if (b != ULLONG_MAX) { zf = z; rk = (int64_t)b; break; }
+      skipped += (int64_t)total;
+    }
+    if (tid0) {
+      A.status[inst] = EB_OK;
+      A.z_found[inst] = zf;
+      A.lexrank[inst] = rk;
+      A.nodes[inst] = zf ? skipped + rk + 1 : skipped;   // 2^n - 1 when none
+      if (A.mask) {
+        uint64_t m = 0;
+        if (zf) {
+          uint64_t r = (uint64_t)rk;
+          int v = 0;
+          for (int j = 0; j < zf; ++j)
+            for (;;) {
+              uint64_t cnt = binom(n - v - 1, zf - j - 1);
+              if (r < cnt) { m |= 1ULL << v; ++v; break; }
+              r -= cnt; ++v;
+            }
+        }
+        A.mask[inst] = m;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+struct RangeArgs {
+  Ctx c;
+  eb_requests req;
+  int n, z;
+  int64_t lo, hi, per;
+  unsigned long long* best;
+  int* status;
+};
+
+// Grid-wide: one level, rank range [lo, hi) split in chunks of `per`.
+__global__ void __launch_bounds__(256) exh_range_kernel(RangeArgs A) {
+  __shared__ Members S;
+  load_members(S, A.c, A.req, 0, A.n);
+  if (S.status) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *A.status = S.status;
+    return;
+  }
+  int64_t nchunks = (A.hi - A.lo + A.per - 1) / A.per;
+  for (int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks;
+       ch += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = A.lo + ch * A.per;
+    if ((unsigned long long)lo > *(volatile unsigned long long*)A.best) break;
+    int64_t hi = lo + A.per < A.hi ? lo + A.per : A.hi;
+    int64_t r = scan_chunk(S, A.z, lo, hi, A.best);
+    if (r >= 0) atomicMin(A.best, (unsigned long long)r);
+  }
+}
+
+}  // namespace
+
+int binom_init(cudaStream_t st) {
+  binom_init_kernel<<<1, EB_MAX_K + 1, 0, st>>>();
+  EB_CUDA(cudaGetLastError());
+  return EB_OK;
+}
+
+int launch_exh_batch(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_ctx,
+                     int64_t n_inst, const int64_t* d_off, const int32_t* d_ci, int64_t req_base,
+                     const eb_requests& d_req, int cap, int32_t* d_status, int32_t* d_z,
+                     int64_t* d_rank, int64_t* d_nodes, uint64_t* d_mask) {
+  if (n_inst <= 0) return EB_OK;
+  BatchArgs A{d_ctxs, n_ctx, n_inst, d_off, d_ci, req_base, d_req, cap, d_status, d_z, d_rank, d_nodes, d_mask};
+  int64_t grid = n_inst < (int64_t)h->num_sms * 8 ? n_inst : (int64_t)h->num_sms * 8;
+  exh_batch_kernel<<<(unsigned)grid, 256, 0, st>>>(A);
+  EB_CUDA(cudaGetLastError());
+  h->launches += 1;
+  return EB_OK;
+}
+
+// One level of one instance over a rank range; synchronous; device pointers.
+int exh_range(eb_handle* h, cudaStream_t st, const eb_context& ctx_host, const eb_requests& d_req,
+              int n, int z, int64_t lo, int64_t hi, unsigned long long* d_best, int* d_status,
+              int64_t* first_rank, int* status) {
+  RangeArgs A;
+  // Ctx is built host-side with the same arithmetic (only products/sums of
+  // config scalars, no libm), mirroring load_ctx.
+  A.c.m.L = ctx_host.layers; A.c.m.d = ctx_host.hidden_dim; A.c.m.heads = ctx_host.head_count;
+  A.c.m.head_dim = ctx_host.head_dim; A.c.m.ffn = ctx_host.ffn_dim; A.c.m.bpp = ctx_host.bytes_per_param;
+  A.c.alpha = ctx_host.alpha; A.c.beta = ctx_host.beta; A.c.delta = ctx_host.delta_ppl;
+  A.c.B_up = ctx_host.uplink_band_hz; A.c.B_dn = ctx_host.downlink_band_hz; A.c.P_dn = ctx_host.downlink_power_w;
+  A.c.N0_up = ctx_host.noise_density_w_hz * ctx_host.uplink_band_hz;
+  A.c.N0_dn = ctx_host.noise_density_w_hz * ctx_host.downlink_band_hz;
+  A.c.T_up = ctx_host.uplink_slot_s; A.c.T_dn = ctx_host.downlink_slot_s;
+  A.c.fbits = (double)ctx_host.bits_per_token;
+  A.c.C = ctx_host.flops_per_s; A.c.M = ctx_host.memory_bytes; A.c.gpus = ctx_host.gpu_count;
+  A.c.has_cap = ctx_host.has_slot_cap != 0; A.c.cap_s = ctx_host.slot_cap_s;
+  A.c.slots = ctx_host.uplink_slot_s + ctx_host.downlink_slot_s;
+  A.req = d_req; A.n = n; A.z = z; A.lo = lo; A.hi = hi;
+  int64_t span = hi - lo;
+  int threads = 256;
+  int64_t max_threads = (int64_t)h->num_sms * 8 * threads;
+  int64_t per = (span + max_threads - 1) / max_threads;
+  if (per < 64) per = 64;
+  A.per = per;
+  A.best = d_best; A.status = d_status;
+  int64_t nchunks = (span + per - 1) / per;
+  int64_t grid = (nchunks + threads - 1) / threads;
+  if (grid > (int64_t)h->num_sms * 8) grid = (int64_t)h->num_sms * 8;
+  if (grid < 1) grid = 1;
+  unsigned long long init = ULLONG_MAX;
+  int zero = 0;
+  EB_CUDA(cudaMemcpyAsync(d_best, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+  EB_CUDA(cudaMemcpyAsync(d_status, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
+  exh_range_kernel<<<(unsigned)grid, threads, 0, st>>>(A);
+  EB_CUDA(cudaGetLastError());
+  h->launches += 1;
+  unsigned long long b;
+  EB_CUDA(cudaMemcpyAsync(&b, d_best, sizeof(b), cudaMemcpyDeviceToHost, st));
+  EB_CUDA(cudaMemcpyAsync(status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  EB_CUDA(cudaStreamSynchronize(st));
+  *first_rank = (b == ULLONG_MAX) ? -1 : (int64_t)b;
+  return EB_OK;
+}
+
+}  // namespace eb

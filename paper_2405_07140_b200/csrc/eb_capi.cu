@@ -1,0 +1,740 @@
+// eb_capi.cu -- extern "C" entry points of include/edgebatch_b200.h.
+//
+// EB_MEM_DEVICE calls launch directly on the handle's stream.  EB_MEM_HOST
+// calls stage through stream-ordered device allocations; eb_dftsp_batch
+// splits large batches into instance chunks pipelined over three streams so
+// host->device copies, the search kernel and device->host copies of
+// neighbouring chunks overlap (pinned caller buffers give true overlap).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "eb_internal.cuh"
+
+namespace eb {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+  return EB_ERR_CUDA;
+}
+
+// launchers defined in the kernel translation units
+size_t dftsp_warp_bytes(int K, int G, bool exact);
+int launch_dftsp(eb_handle*, cudaStream_t, const eb_context*, int, const eb_search_params&, int64_t,
+                 const int64_t*, const int32_t*, int64_t, const eb_requests&, int, const eb_dftsp_result&,
+                 int64_t, int*);
+int launch_dfs_single(eb_handle*, cudaStream_t, int, int, const int32_t*, const int32_t*, const int32_t*,
+                      const double*, const double*, const double*, const double*, const double*, int64_t, int,
+                      double, const eb_search_params&, int32_t*);
+int binom_init(cudaStream_t);
+int launch_exh_batch(eb_handle*, cudaStream_t, const eb_context*, int, int64_t, const int64_t*,
+                     const int32_t*, int64_t, const eb_requests&, int, int32_t*, int32_t*, int64_t*,
+                     int64_t*, uint64_t*);
+int exh_range(eb_handle*, cudaStream_t, const eb_context&, const eb_requests&, int, int, int64_t, int64_t,
+              unsigned long long*, int*, int64_t*, int*);
+int launch_link(eb_handle*, cudaStream_t, const eb_context*, int, const eb_requests&, int64_t,
+                const int32_t*, int32_t*, double*);
+int launch_coeff(eb_handle*, cudaStream_t, const eb_context*, int, int64_t, const int64_t*, const int32_t*,
+                 int64_t, const eb_requests&, const int64_t*, int32_t*, int32_t*, double*, double*);
+int launch_check_direct(eb_handle*, cudaStream_t, const eb_context*, int, const eb_requests&, int64_t,
+                        const int64_t*, const int32_t*, const int32_t*, const int64_t*, int32_t*, uint8_t*,
+                        double*);
+int launch_check_knapsack(eb_handle*, cudaStream_t, int64_t, const int64_t*, const int32_t*, const int32_t*,
+                          const double*, const double*, const double*, const int32_t*, const double*,
+                          uint8_t*);
+int launch_admission(eb_handle*, cudaStream_t, const eb_context*, int, int64_t, int64_t, const int64_t*,
+                     const int32_t*, int64_t, const eb_requests&, int, int, int32_t*, uint8_t*);
+int launch_batch_cost(eb_handle*, cudaStream_t, const eb_context*, int, int64_t, const int64_t*,
+                      const int32_t*, const int32_t*, const int64_t*, const int64_t*, const int32_t*, double*);
+int launch_static_b(eb_handle*, cudaStream_t, const eb_context*, int, const double*, const int64_t*,
+                    const int64_t*, int64_t*);
+int launch_stb(eb_handle*, cudaStream_t, const eb_context*, int, int64_t, const int64_t*, const int32_t*,
+               int64_t, const eb_requests&, const int64_t*, int, int32_t*, uint8_t*);
+int launch_nob(eb_handle*, cudaStream_t, const eb_context*, int, int64_t, const int64_t*, const int32_t*,
+               int64_t, const eb_requests&, const double*, int, const int32_t*, int, double*, int32_t*, int8_t*,
+               double*, int32_t*);
+
+int ensure_dscratch(eb_handle* h, size_t bytes) {
+  if (h->dscratch_bytes >= bytes) return EB_OK;
+  if (h->dscratch) cudaFree(h->dscratch);
+  h->dscratch = nullptr;
+  h->dscratch_bytes = 0;
+  EB_CUDA(cudaMalloc(&h->dscratch, bytes));
+  h->dscratch_bytes = bytes;
+  return EB_OK;
+}
+int ensure_pinned(eb_handle* h, size_t bytes) {
+  if (h->pinned_bytes >= bytes) return EB_OK;
+  if (h->pinned) cudaFreeHost(h->pinned);
+  h->pinned = nullptr;
+  h->pinned_bytes = 0;
+  EB_CUDA(cudaMallocHost(&h->pinned, bytes));
+  h->pinned_bytes = bytes;
+  return EB_OK;
+}
+
+namespace {
+
+// Collects stream-ordered device allocations of one host-memory call.
+struct Stage {
+  eb_handle* h;
+  cudaStream_t st;
+  std::vector<void*> bufs;
+  int err = EB_OK;
+  Stage(eb_handle* hh, cudaStream_t s) : h(hh), st(s) {}
+  ~Stage() { for (void* p : bufs) cudaFreeAsync(p, st); }
+  template <typename T>
+  T* alloc(size_t count) {
+    if (count == 0) count = 1;
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, count * sizeof(T), st);
+    if (e != cudaSuccess) { err = cuda_fail(e, "cudaMallocAsync"); return nullptr; }
+    bufs.push_back(p);
+    return (T*)p;
+  }
+  template <typename T>
+  T* up(const T* host, size_t count) {
+    if (!host) return nullptr;
+    T* d = alloc<T>(count);
+    if (!d) return nullptr;
+    cudaError_t e = cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) { err = cuda_fail(e, "H2D"); return nullptr; }
+    return d;
+  }
+  template <typename T>
+  T* out(const T* host, size_t count) { return host ? alloc<T>(count) : nullptr; }
+  template <typename T>
+  void down(T* host, const T* dev, size_t count) {
+    if (!host || !dev || err) return;
+    cudaError_t e = cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) err = cuda_fail(e, "D2H");
+  }
+  int sync() {
+    if (err) return err;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    return EB_OK;
+  }
+};
+
+eb_requests upload_req(Stage& S, const eb_requests& r, int64_t lo, int64_t n) {
+  eb_requests d;
+  d.id = r.id ? S.up(r.id + lo, n) : nullptr;
+  d.prompt_tokens = S.up(r.prompt_tokens + lo, n);
+  d.output_tokens = S.up(r.output_tokens + lo, n);
+  d.deadline_s = r.deadline_s ? S.up(r.deadline_s + lo, n) : nullptr;
+  d.waiting_s = r.waiting_s ? S.up(r.waiting_s + lo, n) : nullptr;
+  d.tolerance = r.tolerance ? S.up(r.tolerance + lo, n) : nullptr;
+  d.channel_gain = r.channel_gain ? S.up(r.channel_gain + lo, n) : nullptr;
+  d.uplink_power_w = r.uplink_power_w ? S.up(r.uplink_power_w + lo, n) : nullptr;
+  return d;
+}
+
+bool req_complete(const eb_requests& r, bool need_tol) {
+  return r.id && r.prompt_tokens && r.output_tokens && r.deadline_s && r.waiting_s && r.channel_gain &&
+         r.uplink_power_w && (!need_tol || r.tolerance);
+}
+
+// Exact int64 bound for every FLOP/byte count a context can produce on
+// instances of at most kmax requests with prompts/outputs <= smax/nmax.
+bool ctx_fits_int64(const eb_context& c, int64_t kmax, int64_t smax, int64_t nmax) {
+  typedef __int128 I;
+  I L = c.layers, d = c.hidden_dim, f = c.ffn_dim, bpp = c.bytes_per_param;
+  I s = smax, n = nmax, k = kmax;
+  I fi = L * (6 * s * d * d + 4 * s * s * d + 2 * s * d * d + 4 * s * d * f);
+  I far = L * n * (8 * d * d + 4 * s * d + 4 * d * f + 2 * d * n);
+  I w = L * (4 * bpp * d * (I)c.head_dim * (I)c.head_count + 2 * bpp * d * f);
+  I mem = w + 2 * bpp * L * d * (s + n) * k;
+  I lim = ((I)1) << 62;
+  return c.layers >= 0 && c.hidden_dim > 0 && c.ffn_dim > 0 && k * (fi + far) < lim && mem < lim && w < lim;
+}
+
+}  // namespace
+}  // namespace eb
+
+using namespace eb;
+
+extern "C" {
+
+int32_t eb_abi_version(void) { return EB_ABI_VERSION; }
+
+const char* eb_status_string(int32_t s) {
+  switch (s) {
+    case EB_OK: return "ok";
+    case EB_ERR_INVALID_ARG: return "invalid argument";
+    case EB_ERR_CUDA: return "CUDA error";
+    case EB_ERR_K_TOO_LARGE: return "instance too large";
+    case EB_ERR_TOO_MANY_CLASSES: return "too many output-length classes";
+    case EB_ERR_NO_DEVICE: return "no CUDA device";
+    case EB_ERR_WEIGHTS_DO_NOT_FIT: return "weights do not fit";
+    case EB_ERR_UPLINK_EFF_ZERO: return "uplink spectral efficiency is zero";
+    case EB_ERR_DOWNLINK_EFF_ZERO: return "downlink spectral efficiency is zero";
+    case EB_ERR_OFF_LADDER: return "output length not on the class ladder";
+    case EB_ERR_REVERIFY: return "reduced-form solution failed direct re-verification";
+    case EB_ERR_DUPLICATE_ID: return "duplicate request id";
+    case EB_ERR_CAP_EXCEEDED: return "pool size exceeds the exhaustive cap";
+    case EB_ERR_OVERFLOW: return "integer cost model would overflow int64";
+    case EB_ERR_BAD_MODE: return "unknown exhaustive mode";
+    case EB_ERR_PADDED_TOO_SMALL: return "padded_len must cover every candidate prompt";
+    default: return "unknown status";
+  }
+}
+
+const char* eb_last_error(void) { return g_err; }
+
+int32_t eb_handle_create(int32_t device, eb_handle** out) {
+  if (!out) return EB_ERR_INVALID_ARG;
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    set_error("no CUDA device: %s", e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
+    return EB_ERR_NO_DEVICE;
+  }
+  if (device < 0 || device >= count) return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(device));
+  eb_handle* h = new eb_handle();
+  memset(h, 0, sizeof(*h));
+  h->device = device;
+  EB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  h->own_stream = true;
+  for (int i = 0; i < 3; ++i) {
+    EB_CUDA(cudaStreamCreateWithFlags(&h->pipe[i], cudaStreamNonBlocking));
+    EB_CUDA(cudaEventCreateWithFlags(&h->ev[i], cudaEventDisableTiming));
+  }
+  EB_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  int st = binom_init(h->stream);
+  if (st) { delete h; return st; }
+  EB_CUDA(cudaStreamSynchronize(h->stream));
+  h->launches = 1;
+  *out = h;
+  return EB_OK;
+}
+
+int32_t eb_handle_destroy(eb_handle* h) {
+  if (!h) return EB_OK;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  if (h->own_stream) cudaStreamDestroy(h->stream);
+  for (int i = 0; i < 3; ++i) { cudaStreamDestroy(h->pipe[i]); cudaEventDestroy(h->ev[i]); }
+  if (h->dscratch) cudaFree(h->dscratch);
+  if (h->pinned) cudaFreeHost(h->pinned);
+  delete h;
+  return EB_OK;
+}
+
+int32_t eb_handle_set_stream(eb_handle* h, void* stream) {
+  if (!h) return EB_ERR_INVALID_ARG;
+  if (h->own_stream) cudaStreamDestroy(h->stream);
+  h->stream = (cudaStream_t)stream;
+  h->own_stream = false;
+  return EB_OK;
+}
+
+int32_t eb_synchronize(eb_handle* h) {
+  if (!h) return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  EB_CUDA(cudaStreamSynchronize(h->stream));
+  for (int i = 0; i < 3; ++i) EB_CUDA(cudaStreamSynchronize(h->pipe[i]));
+  return EB_OK;
+}
+
+int64_t eb_kernel_launches(eb_handle* h) { return h ? h->launches : -1; }
+
+// ---------------------------------------------------------------------------
+int32_t eb_dftsp_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_search_params* prm,
+                       const eb_batch* b, eb_dftsp_result* out, int32_t mem) {
+  if (!h || !ctxs || n_ctx < 1 || !prm || !b || !out || !out->status || !out->z_found ||
+      !out->nodes_visited || !out->nodes_pruned || b->n_inst < 0 || !b->offsets)
+    return EB_ERR_INVALID_ARG;
+  if (prm->ladder_len < 0 || prm->ladder_len > EB_MAX_CLASSES) return EB_ERR_INVALID_ARG;
+  if (!req_complete(b->req, false)) return EB_ERR_INVALID_ARG;
+  if (prm->collect_trajectory && (!out->traj || !out->traj_offsets)) return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (b->n_inst == 0) return EB_OK;
+
+  if (mem == EB_MEM_DEVICE) {
+    int K = b->k_max;
+    if (K < 1 || K > EB_MAX_K) return EB_ERR_INVALID_ARG;
+    int st = ensure_dscratch(h, 256);
+    if (st) return st;
+    return launch_dftsp(h, h->stream, ctxs, n_ctx, *prm, b->n_inst, b->offsets, b->ctx_index, 0, b->req, K,
+                        *out, 0, (int*)h->dscratch);
+  }
+  if (mem != EB_MEM_HOST) return EB_ERR_INVALID_ARG;
+
+  // ---- host memory: validate, then pipeline instance chunks -------------
+  const int64_t n = b->n_inst;
+  int K = b->k_max;
+  int64_t smax = 1, nmax = 1;
+  {
+    int kk = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t sz = b->offsets[i + 1] - b->offsets[i];
+      if (sz < 0) return EB_ERR_INVALID_ARG;
+      if (sz > kk) kk = (int)(sz > EB_MAX_K ? EB_MAX_K + 1 : sz);
+    }
+    if (K <= 0) K = kk;
+    if (K > EB_MAX_K) K = EB_MAX_K;
+    if (K < 1) K = 1;
+    for (int64_t r = b->offsets[0]; r < b->offsets[n]; ++r) {
+      if (b->req.prompt_tokens[r] > smax) smax = b->req.prompt_tokens[r];
+      if (b->req.output_tokens[r] > nmax) nmax = b->req.output_tokens[r];
+    }
+    for (int c = 0; c < n_ctx; ++c)
+      if (!ctx_fits_int64(ctxs[c], K, smax, nmax)) {
+        set_error("context %d: exact FLOP/byte counts exceed int64 at K=%d, prompt<=%lld, output<=%lld", c, K,
+                  (long long)smax, (long long)nmax);
+        return EB_ERR_OVERFLOW;
+      }
+  }
+  // Chunking: ~8 chunks for big batches, never below 8192 instances.
+  int64_t chunk = (n + 7) / 8;
+  if (chunk < 8192) chunk = 8192;
+  const int nchunks = (int)((n + chunk - 1) / chunk);
+  // The pipeline streams fork from / join back into the handle's stream so
+  // events a caller records on that stream bracket the whole host->host call.
+  EB_CUDA(cudaEventRecord(h->ev[0], h->stream));
+  for (int i = 0; i < 3; ++i) EB_CUDA(cudaStreamWaitEvent(h->pipe[i], h->ev[0], 0));
+  // context table once per pipe stream (tiny)
+  std::vector<Stage*> stages;
+  int rc = EB_OK;
+  eb_context* d_ctx[3] = {nullptr, nullptr, nullptr};
+  for (int c = 0; c < nchunks && rc == EB_OK; ++c) {
+    cudaStream_t st = h->pipe[c % 3];
+    Stage* S = new Stage(h, st);
+    stages.push_back(S);
+    if (!d_ctx[c % 3]) d_ctx[c % 3] = S->up(ctxs, (size_t)n_ctx);
+    const int64_t i0 = c * chunk, i1 = (i0 + chunk < n) ? i0 + chunk : n, ni = i1 - i0;
+    const int64_t R0 = b->offsets[i0], R1 = b->offsets[i1], nr = R1 - R0;
+    const int64_t* d_off = S->up(b->offsets + i0, (size_t)ni + 1);
+    const int32_t* d_ci = b->ctx_index ? S->up(b->ctx_index + i0, (size_t)ni) : nullptr;
+    eb_requests d_req = upload_req(*S, b->req, R0, nr);
+    eb_dftsp_result d_out;
+    memset(&d_out, 0, sizeof(d_out));
+    d_out.status = S->alloc<int32_t>(ni);
+    d_out.error_index = S->out(out->error_index, ni);
+    d_out.z_found = S->alloc<int32_t>(ni);
+    d_out.nodes_visited = S->alloc<int64_t>(ni);
+    d_out.nodes_pruned = S->alloc<int64_t>(ni);
+    d_out.n_classes = S->out(out->n_classes, ni);
+    d_out.counts = S->out(out->counts, ni * EB_MAX_CLASSES);
+    d_out.class_lengths = S->out(out->class_lengths, ni * EB_MAX_CLASSES);
+    d_out.solution = S->out(out->solution, nr);
+    d_out.metrics = S->out(out->metrics, ni * EB_N_METRICS);
+    int64_t T0 = 0;
+    if (prm->collect_trajectory) {
+      T0 = out->traj_offsets[i0];
+      int64_t nt = out->traj_offsets[i1] - T0;
+      d_out.traj_offsets = S->up(out->traj_offsets + i0, (size_t)ni + 1);
+      d_out.traj = S->alloc<int64_t>((size_t)nt * 4);
+      d_out.traj_len = S->out(out->traj_len, ni);
+    }
+    int* d_counter = S->alloc<int>(1);
+    if (S->err) { rc = S->err; break; }
+    rc = launch_dftsp(h, st, d_ctx[c % 3], n_ctx, *prm, ni, d_off, d_ci, R0, d_req, K, d_out, T0, d_counter);
+    if (rc) break;
+    S->down(out->status + i0, d_out.status, ni);
+    S->down(out->error_index ? out->error_index + i0 : nullptr, d_out.error_index, ni);
+    S->down(out->z_found + i0, d_out.z_found, ni);
+    S->down(out->nodes_visited + i0, d_out.nodes_visited, ni);
+    S->down(out->nodes_pruned + i0, d_out.nodes_pruned, ni);
+    S->down(out->n_classes ? out->n_classes + i0 : nullptr, d_out.n_classes, ni);
+    S->down(out->counts ? out->counts + i0 * EB_MAX_CLASSES : nullptr, d_out.counts, ni * EB_MAX_CLASSES);
+    S->down(out->class_lengths ? out->class_lengths + i0 * EB_MAX_CLASSES : nullptr, d_out.class_lengths,
+            ni * EB_MAX_CLASSES);
+    S->down(out->solution ? out->solution + R0 : nullptr, d_out.solution, nr);
+    S->down(out->metrics ? out->metrics + i0 * EB_N_METRICS : nullptr, d_out.metrics, ni * EB_N_METRICS);
+    if (prm->collect_trajectory) {
+      S->down(out->traj + 4 * T0, d_out.traj, (out->traj_offsets[i1] - T0) * 4);
+      S->down(out->traj_len ? out->traj_len + i0 : nullptr, d_out.traj_len, ni);
+    }
+    if (S->err) { rc = S->err; break; }
+  }
+  for (Stage* S : stages) {
+    int s2 = S->sync();
+    if (!rc) rc = s2;
+  }
+  for (Stage* S : stages) delete S;   // stream-ordered frees
+  for (int i = 0; i < 3; ++i) {
+    cudaEventRecord(h->ev[i], h->pipe[i]);
+    cudaStreamWaitEvent(h->stream, h->ev[i], 0);
+  }
+  for (int i = 0; i < 3; ++i) cudaStreamSynchronize(h->pipe[i]);
+  return rc;
+}
+
+int32_t eb_dfs_single(eb_handle* h, int32_t z, int32_t n_cls, const int32_t* sizes, const int32_t* lengths,
+                      const int32_t* prompt, const double* k_up, const double* k_down, const double* deadline_s,
+                      const double* waiting_s, const double coeff[8], int64_t padded_len, int32_t has_tau_min,
+                      double tau_min, const eb_search_params* prm, int32_t* out_found, int32_t* out_counts,
+                      int64_t* out_visited, int64_t* out_pruned) {
+  if (!h || !prm || n_cls < 0 || n_cls > EB_MAX_CLASSES || (n_cls > 0 && (!sizes || !lengths)) || !coeff ||
+      !out_found || !out_visited || !out_pruned)
+    return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  int total = 0;
+  for (int k = 0; k < n_cls; ++k) {
+    if (sizes[k] < 0) return EB_ERR_INVALID_ARG;
+    total += sizes[k];
+  }
+  if (total > EB_MAX_K) return EB_ERR_K_TOO_LARGE;
+  if (total > 0 && (!prompt || !k_up || !k_down || !deadline_s || !waiting_s)) return EB_ERR_INVALID_ARG;
+  const size_t nm = (size_t)(total > 0 ? total : 1), nc = (size_t)(n_cls > 0 ? n_cls : 1);
+  Stage S(h, h->stream);
+  int32_t* d_sizes = n_cls ? S.up(sizes, nc) : S.alloc<int32_t>(1);
+  int32_t* d_len = n_cls ? S.up(lengths, nc) : S.alloc<int32_t>(1);
+  int32_t* d_pr = total ? S.up(prompt, nm) : S.alloc<int32_t>(1);
+  double* d_ku = total ? S.up(k_up, nm) : S.alloc<double>(1);
+  double* d_kd = total ? S.up(k_down, nm) : S.alloc<double>(1);
+  double* d_dl = total ? S.up(deadline_s, nm) : S.alloc<double>(1);
+  double* d_wt = total ? S.up(waiting_s, nm) : S.alloc<double>(1);
+  double* d_co = S.up(coeff, 8);
+  int32_t* d_res = S.alloc<int32_t>(2 + EB_MAX_CLASSES + 4);
+  if (S.err) return S.err;
+  int rc = launch_dfs_single(h, h->stream, z, n_cls, d_sizes, d_len, d_pr, d_ku, d_kd, d_dl, d_wt, d_co,
+                             padded_len, has_tau_min, tau_min, *prm, d_res);
+  if (rc) return rc;
+  int32_t res[2 + EB_MAX_CLASSES + 4];
+  S.down(res, d_res, 2 + EB_MAX_CLASSES + 4);
+  rc = S.sync();
+  if (rc) return rc;
+  *out_found = res[0];
+  if (out_counts)
+    for (int k = 0; k < n_cls; ++k) out_counts[k] = res[2 + k];
+  int64_t v, p;
+  memcpy(&v, &res[2 + EB_MAX_CLASSES], 8);
+  memcpy(&p, &res[2 + EB_MAX_CLASSES + 2], 8);
+  *out_visited = v;
+  *out_pruned = p;
+  return EB_OK;
+}
+
+int32_t eb_exhaustive_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_batch* b, int32_t cap,
+                            int32_t* status, int32_t* z_found, int64_t* lexrank, int64_t* nodes_visited,
+                            uint64_t* subset_mask, int32_t mem) {
+  if (!h || !ctxs || n_ctx < 1 || !b || !b->offsets || !status || !z_found || !lexrank || !nodes_visited ||
+      b->n_inst < 0 || !req_complete(b->req, false))
+    return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (b->n_inst == 0) return EB_OK;
+  if (mem == EB_MEM_DEVICE)
+    return launch_exh_batch(h, h->stream, ctxs, n_ctx, b->n_inst, b->offsets, b->ctx_index, 0, b->req, cap,
+                            status, z_found, lexrank, nodes_visited, subset_mask);
+  const int64_t n = b->n_inst, R0 = b->offsets[0], nr = b->offsets[n] - R0;
+  Stage S(h, h->stream);
+  const eb_context* d_ctx = S.up(ctxs, (size_t)n_ctx);
+  const int64_t* d_off = S.up(b->offsets, (size_t)n + 1);
+  const int32_t* d_ci = b->ctx_index ? S.up(b->ctx_index, (size_t)n) : nullptr;
+  eb_requests d_req = upload_req(S, b->req, R0, nr);
+  int32_t* d_st = S.alloc<int32_t>(n);
+  int32_t* d_z = S.alloc<int32_t>(n);
+  int64_t* d_rk = S.alloc<int64_t>(n);
+  int64_t* d_nd = S.alloc<int64_t>(n);
+  uint64_t* d_mk = S.out(subset_mask, n);
+  if (S.err) return S.err;
+  int rc = launch_exh_batch(h, h->stream, d_ctx, n_ctx, n, d_off, d_ci, R0, d_req, cap, d_st, d_z, d_rk, d_nd,
+                            d_mk);
+  if (rc) return rc;
+  S.down(status, d_st, n);
+  S.down(z_found, d_z, n);
+  S.down(lexrank, d_rk, n);
+  S.down(nodes_visited, d_nd, n);
+  S.down(subset_mask, d_mk, n);
+  return S.sync();
+}
+
+int32_t eb_exhaustive_level_range(eb_handle* h, const eb_context* ctx, int32_t k, const eb_requests* req,
+                                  int32_t z, int64_t rank_lo, int64_t rank_hi, int64_t* first_rank) {
+  if (!h || !ctx || !req || !first_rank || k < 1 || k > EB_MAX_K || z < 1 || z > k || rank_lo < 0 ||
+      rank_hi < rank_lo || !req_complete(*req, false))
+    return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  *first_rank = -1;
+  if (rank_hi == rank_lo) return EB_OK;
+  Stage S(h, h->stream);
+  eb_requests d_req = upload_req(S, *req, 0, k);
+  unsigned long long* d_best = S.alloc<unsigned long long>(1);
+  int* d_status = S.alloc<int>(1);
+  if (S.err) return S.err;
+  int status = 0;
+  int rc = exh_range(h, h->stream, *ctx, d_req, k, z, rank_lo, rank_hi, d_best, d_status, first_rank, &status);
+  if (rc) return rc;
+  rc = S.sync();
+  if (rc) return rc;
+  return status ? status : EB_OK;
+}
+
+int32_t eb_check_direct_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_requests* req,
+                              int64_t n_rows, int64_t n_sub, const int64_t* sub_off, const int32_t* members,
+                              const int32_t* sub_ctx, const int64_t* padded_len, int32_t* status,
+                              uint8_t* out_ok, double* out_metrics, int32_t mem) {
+  if (!h || !ctxs || n_ctx < 1 || !req || n_sub < 0 || !sub_off || !padded_len || !status || !out_ok ||
+      !req_complete(*req, false))
+    return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (n_sub == 0) return EB_OK;
+  if (mem == EB_MEM_DEVICE)
+    return launch_check_direct(h, h->stream, ctxs, n_ctx, *req, n_sub, sub_off, members, sub_ctx, padded_len,
+                               status, out_ok, out_metrics);
+  int64_t nm = sub_off[n_sub] - sub_off[0];
+  if (sub_off[0] != 0 || nm < 0) return EB_ERR_INVALID_ARG;
+  Stage S(h, h->stream);
+  const eb_context* d_ctx = S.up(ctxs, (size_t)n_ctx);
+  eb_requests d_req = upload_req(S, *req, 0, n_rows);
+  const int64_t* d_off = S.up(sub_off, (size_t)n_sub + 1);
+  const int32_t* d_mem = S.up(members, (size_t)nm);
+  const int32_t* d_sc = sub_ctx ? S.up(sub_ctx, (size_t)n_sub) : nullptr;
+  const int64_t* d_pad = S.up(padded_len, (size_t)n_sub);
+  int32_t* d_st = S.alloc<int32_t>(n_sub);
+  uint8_t* d_ok = S.alloc<uint8_t>(n_sub);
+  double* d_met = S.out(out_metrics, (size_t)n_sub * 4);
+  if (S.err) return S.err;
+  int rc = launch_check_direct(h, h->stream, d_ctx, n_ctx, d_req, n_sub, d_off, d_mem, d_sc, d_pad, d_st, d_ok,
+                               d_met);
+  if (rc) return rc;
+  S.down(status, d_st, n_sub);
+  S.down(out_ok, d_ok, n_sub);
+  S.down(out_metrics, d_met, (size_t)n_sub * 4);
+  return S.sync();
+}
+
+int32_t eb_check_knapsack_batch(eb_handle* h, int64_t n_sub, const int64_t* sub_off, const int32_t* prompt,
+                                const int32_t* output, const double* k_up, const double* k_down,
+                                const double* coeff, const int32_t* z, const double* tau_min, uint8_t* out_ok,
+                                int32_t mem) {
+  if (!h || n_sub < 0 || !sub_off || !coeff || !z || !tau_min || !out_ok) return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (n_sub == 0) return EB_OK;
+  if (mem == EB_MEM_DEVICE)
+    return launch_check_knapsack(h, h->stream, n_sub, sub_off, prompt, output, k_up, k_down, coeff, z, tau_min,
+                                 out_ok);
+  int64_t nm = sub_off[n_sub];
+  if (sub_off[0] != 0 || nm < 0) return EB_ERR_INVALID_ARG;
+  Stage S(h, h->stream);
+  const int64_t* d_off = S.up(sub_off, (size_t)n_sub + 1);
+  const int32_t* d_p = S.up(prompt, (size_t)nm);
+  const int32_t* d_o = S.up(output, (size_t)nm);
+  const double* d_ku = S.up(k_up, (size_t)nm);
+  const double* d_kd = S.up(k_down, (size_t)nm);
+  const double* d_co = S.up(coeff, (size_t)n_sub * 6);
+  const int32_t* d_z = S.up(z, (size_t)n_sub);
+  const double* d_tm = S.up(tau_min, (size_t)n_sub);
+  uint8_t* d_ok = S.alloc<uint8_t>(n_sub);
+  if (S.err) return S.err;
+  int rc = launch_check_knapsack(h, h->stream, n_sub, d_off, d_p, d_o, d_ku, d_kd, d_co, d_z, d_tm, d_ok);
+  if (rc) return rc;
+  S.down(out_ok, d_ok, n_sub);
+  return S.sync();
+}
+
+int32_t eb_coefficients_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_batch* b,
+                              const int64_t* padded_len, int32_t* status, int32_t* error_index,
+                              double* out_scalar, double* out_req, int32_t mem) {
+  if (!h || !ctxs || n_ctx < 1 || !b || !b->offsets || !status || !out_scalar || !out_req ||
+      !req_complete(b->req, false))
+    return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (b->n_inst == 0) return EB_OK;
+  if (mem == EB_MEM_DEVICE)
+    return launch_coeff(h, h->stream, ctxs, n_ctx, b->n_inst, b->offsets, b->ctx_index, 0, b->req, padded_len,
+                        status, error_index, out_scalar, out_req);
+  const int64_t n = b->n_inst, R0 = b->offsets[0], nr = b->offsets[n] - R0;
+  Stage S(h, h->stream);
+  const eb_context* d_ctx = S.up(ctxs, (size_t)n_ctx);
+  const int64_t* d_off = S.up(b->offsets, (size_t)n + 1);
+  const int32_t* d_ci = b->ctx_index ? S.up(b->ctx_index, (size_t)n) : nullptr;
+  eb_requests d_req = upload_req(S, b->req, R0, nr);
+  const int64_t* d_pad = padded_len ? S.up(padded_len, (size_t)n) : nullptr;
+  int32_t* d_st = S.alloc<int32_t>(n);
+  int32_t* d_err = S.out(error_index, n);
+  double* d_sc = S.alloc<double>((size_t)n * 6);
+  double* d_rq = S.alloc<double>((size_t)nr * 4);
+  if (S.err) return S.err;
+  int rc = launch_coeff(h, h->stream, d_ctx, n_ctx, n, d_off, d_ci, R0, d_req, d_pad, d_st, d_err, d_sc, d_rq);
+  if (rc) return rc;
+  S.down(status, d_st, n);
+  S.down(error_index, d_err, n);
+  S.down(out_scalar, d_sc, (size_t)n * 6);
+  S.down(out_req + 4 * R0, d_rq, (size_t)nr * 4);
+  return S.sync();
+}
+
+int32_t eb_link_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_requests* req, int64_t n,
+                      const int32_t* req_ctx, int32_t* status, double* out, int32_t mem) {
+  if (!h || !ctxs || n_ctx < 1 || !req || n < 0 || !status || !out || !req->channel_gain ||
+      !req->uplink_power_w || !req->prompt_tokens || !req->output_tokens)
+    return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (n == 0) return EB_OK;
+  if (mem == EB_MEM_DEVICE) return launch_link(h, h->stream, ctxs, n_ctx, *req, n, req_ctx, status, out);
+  Stage S(h, h->stream);
+  const eb_context* d_ctx = S.up(ctxs, (size_t)n_ctx);
+  eb_requests d_req;
+  memset(&d_req, 0, sizeof(d_req));
+  d_req.prompt_tokens = S.up(req->prompt_tokens, n);
+  d_req.output_tokens = S.up(req->output_tokens, n);
+  d_req.channel_gain = S.up(req->channel_gain, n);
+  d_req.uplink_power_w = S.up(req->uplink_power_w, n);
+  const int32_t* d_rc = req_ctx ? S.up(req_ctx, (size_t)n) : nullptr;
+  int32_t* d_st = S.alloc<int32_t>(n);
+  double* d_out = S.alloc<double>((size_t)n * 6);
+  if (S.err) return S.err;
+  int rc = launch_link(h, h->stream, d_ctx, n_ctx, d_req, n, d_rc, d_st, d_out);
+  if (rc) return rc;
+  S.down(status, d_st, n);
+  S.down(out, d_out, (size_t)n * 6);
+  return S.sync();
+}
+
+int32_t eb_admission_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_batch* b,
+                           int32_t accuracy_check, int32_t prefilter, int32_t* status, uint8_t* out_keep,
+                           int32_t mem) {
+  if (!h || !ctxs || n_ctx < 1 || !b || !b->offsets || !status || !out_keep ||
+      (accuracy_check && !b->req.tolerance) || (prefilter && !req_complete(b->req, false)))
+    return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (b->n_inst == 0) return EB_OK;
+  if (mem == EB_MEM_DEVICE)
+    return launch_admission(h, h->stream, ctxs, n_ctx, b->n_inst, b->n_req, b->offsets, b->ctx_index, 0,
+                            b->req, accuracy_check, prefilter, status, out_keep);
+  const int64_t n = b->n_inst, R0 = b->offsets[0], nr = b->offsets[n] - R0;
+  Stage S(h, h->stream);
+  const eb_context* d_ctx = S.up(ctxs, (size_t)n_ctx);
+  const int64_t* d_off = S.up(b->offsets, (size_t)n + 1);
+  const int32_t* d_ci = b->ctx_index ? S.up(b->ctx_index, (size_t)n) : nullptr;
+  eb_requests d_req = upload_req(S, b->req, R0, nr);
+  int32_t* d_st = S.alloc<int32_t>(nr);
+  uint8_t* d_k = S.alloc<uint8_t>(nr);
+  if (S.err) return S.err;
+  int rc = launch_admission(h, h->stream, d_ctx, n_ctx, n, nr, d_off, d_ci, R0, d_req, accuracy_check, prefilter,
+                            d_st, d_k);
+  if (rc) return rc;
+  S.down(status + R0, d_st, nr);
+  S.down(out_keep + R0, d_k, nr);
+  return S.sync();
+}
+
+int32_t eb_batch_cost_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, int64_t n_plans,
+                            const int64_t* plan_off, const int32_t* prompt, const int32_t* output,
+                            const int64_t* padded_len, const int64_t* weight_copies, const int32_t* plan_ctx,
+                            double* out, int32_t mem) {
+  if (!h || !ctxs || n_ctx < 1 || n_plans < 0 || !plan_off || !padded_len || !out) return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (n_plans == 0) return EB_OK;
+  if (mem == EB_MEM_DEVICE)
+    return launch_batch_cost(h, h->stream, ctxs, n_ctx, n_plans, plan_off, prompt, output, padded_len,
+                             weight_copies, plan_ctx, out);
+  int64_t ne = plan_off[n_plans];
+  if (plan_off[0] != 0 || ne < 0) return EB_ERR_INVALID_ARG;
+  Stage S(h, h->stream);
+  const eb_context* d_ctx = S.up(ctxs, (size_t)n_ctx);
+  const int64_t* d_off = S.up(plan_off, (size_t)n_plans + 1);
+  const int32_t* d_p = S.up(prompt, (size_t)ne);
+  const int32_t* d_o = S.up(output, (size_t)ne);
+  const int64_t* d_pad = S.up(padded_len, (size_t)n_plans);
+  const int64_t* d_cp = weight_copies ? S.up(weight_copies, (size_t)n_plans) : nullptr;
+  const int32_t* d_pc = plan_ctx ? S.up(plan_ctx, (size_t)n_plans) : nullptr;
+  double* d_out = S.alloc<double>((size_t)n_plans * 2);
+  if (S.err) return S.err;
+  int rc = launch_batch_cost(h, h->stream, d_ctx, n_ctx, n_plans, d_off, d_p, d_o, d_pad, d_cp, d_pc, d_out);
+  if (rc) return rc;
+  S.down(out, d_out, (size_t)n_plans * 2);
+  return S.sync();
+}
+
+int32_t eb_static_batch_size_batch(eb_handle* h, const eb_context* ctxs, int32_t n, const double* slot_s,
+                                   const int64_t* s_max, const int64_t* n_max, int64_t* out_b, int32_t mem) {
+  if (!h || !ctxs || n < 0 || !slot_s || !s_max || !n_max || !out_b) return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (n == 0) return EB_OK;
+  if (mem == EB_MEM_DEVICE) return launch_static_b(h, h->stream, ctxs, n, slot_s, s_max, n_max, out_b);
+  Stage S(h, h->stream);
+  const eb_context* d_ctx = S.up(ctxs, (size_t)n);
+  const double* d_sl = S.up(slot_s, (size_t)n);
+  const int64_t* d_s = S.up(s_max, (size_t)n);
+  const int64_t* d_n = S.up(n_max, (size_t)n);
+  int64_t* d_out = S.alloc<int64_t>(n);
+  if (S.err) return S.err;
+  int rc = launch_static_b(h, h->stream, d_ctx, n, d_sl, d_s, d_n, d_out);
+  if (rc) return rc;
+  S.down(out_b, d_out, (size_t)n);
+  return S.sync();
+}
+
+int32_t eb_stb_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_batch* b, const int64_t* bsz,
+                     int32_t accuracy_check, int32_t* status, uint8_t* out_sel, int32_t mem) {
+  if (!h || !ctxs || n_ctx < 1 || !b || !b->offsets || !bsz || !status || !out_sel) return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (b->n_inst == 0) return EB_OK;
+  if (mem == EB_MEM_DEVICE)
+    return launch_stb(h, h->stream, ctxs, n_ctx, b->n_inst, b->offsets, b->ctx_index, 0, b->req, bsz,
+                      accuracy_check, status, out_sel);
+  const int64_t n = b->n_inst, R0 = b->offsets[0], nr = b->offsets[n] - R0;
+  Stage S(h, h->stream);
+  const eb_context* d_ctx = S.up(ctxs, (size_t)n_ctx);
+  const int64_t* d_off = S.up(b->offsets, (size_t)n + 1);
+  const int32_t* d_ci = b->ctx_index ? S.up(b->ctx_index, (size_t)n) : nullptr;
+  eb_requests d_req = upload_req(S, b->req, R0, nr);
+  const int64_t* d_b = S.up(bsz, (size_t)n);
+  int32_t* d_st = S.alloc<int32_t>(n);
+  uint8_t* d_sel = S.alloc<uint8_t>(nr);
+  if (S.err) return S.err;
+  int rc = launch_stb(h, h->stream, d_ctx, n_ctx, n, d_off, d_ci, R0, d_req, d_b, accuracy_check, d_st, d_sel);
+  if (rc) return rc;
+  S.down(status, d_st, n);
+  S.down(out_sel + R0, d_sel, nr);
+  return S.sync();
+}
+
+int32_t eb_nob_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_batch* b, const double* now,
+                     int32_t accuracy_check, const int32_t* n_dev, int32_t max_dev, double* busy_until, int32_t* status,
+                     int8_t* out_action, double* out_completion, int32_t* out_order, int32_t mem) {
+  if (!h || !ctxs || n_ctx < 1 || !b || !b->offsets || !now || max_dev < 1 || !busy_until || !status ||
+      !out_action || !out_completion || !out_order)
+    return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (b->n_inst == 0) return EB_OK;
+  if (mem == EB_MEM_DEVICE)
+    return launch_nob(h, h->stream, ctxs, n_ctx, b->n_inst, b->offsets, b->ctx_index, 0, b->req, now,
+                      accuracy_check, n_dev, max_dev, busy_until, status, out_action, out_completion, out_order);
+  const int64_t n = b->n_inst, R0 = b->offsets[0], nr = b->offsets[n] - R0;
+  Stage S(h, h->stream);
+  const eb_context* d_ctx = S.up(ctxs, (size_t)n_ctx);
+  const int64_t* d_off = S.up(b->offsets, (size_t)n + 1);
+  const int32_t* d_ci = b->ctx_index ? S.up(b->ctx_index, (size_t)n) : nullptr;
+  eb_requests d_req = upload_req(S, b->req, R0, nr);
+  const double* d_now = S.up(now, (size_t)n);
+  const int32_t* d_nd = n_dev ? S.up(n_dev, (size_t)n) : nullptr;
+  double* d_busy = S.up(busy_until, (size_t)n * max_dev);
+  int32_t* d_st = S.alloc<int32_t>(n);
+  int8_t* d_act = S.alloc<int8_t>(nr);
+  double* d_cmp = S.alloc<double>(nr);
+  int32_t* d_ord = S.alloc<int32_t>(nr);
+  if (S.err) return S.err;
+  int rc = launch_nob(h, h->stream, d_ctx, n_ctx, n, d_off, d_ci, R0, d_req, d_now, accuracy_check, d_nd, max_dev,
+                      d_busy, d_st, d_act, d_cmp, d_ord);
+  if (rc) return rc;
+  S.down(busy_until, d_busy, (size_t)n * max_dev);
+  S.down(status, d_st, n);
+  S.down(out_action + R0, d_act, nr);
+  S.down(out_completion + R0, d_cmp, nr);
+  S.down(out_order + R0, d_ord, nr);
+  return S.sync();
+}
+
+}  // extern "C"

@@ -1,0 +1,841 @@
+// eb_dftsp.cu -- K3: instance-parallel DFTSP (reference dftsp.py:237-285).
+//
+// One warp per scheduling instance (persistent warps pull instances from an
+// atomic queue).  Inside the warp:
+//   setup   lanes = requests: coefficients (feasibility.py:133-167, device
+//           glibc-log2 port), normalized-deadline order (dftsp.py:257),
+//           output-length classes and within-class uplink order
+//           (dftsp.py:54-82), then lanes = (d, class) pairs build every
+//           pool-width-d prefix table (SearchTables.build dftsp.py:110-132)
+//           in shared memory;
+//   search  lanes = dfs calls.  The reference walks calls (z from K down, d
+//           from z up) until the first success; here the 32 lanes run 32
+//           consecutive calls of that sequence concurrently, each lane a
+//           literal restatement of the dfs node loop (dftsp.py:153-234)
+//           with its accumulators in registers (recomputed on backtrack
+//           from the packed count stack, bit-identically).  Lanes pull the
+//           next call when they finish; a warp ballot/min keeps the first
+//           successful call in sequence order, aborts speculative calls
+//           behind it, and folds node counts in sequence order -- so
+//           nodes_visited / nodes_pruned equal the reference's totals.
+//   finish  recover_subset + check_direct re-verification (dftsp.py:276),
+//           solution sorted by id, derived metrics.
+#include <climits>
+
+#include "eb_internal.cuh"
+
+namespace eb {
+namespace {
+
+constexpr int RING = 64;  // in-flight window of dfs calls per warp
+
+struct __align__(8) LevelInfo {
+  uint16_t off;       // table offset (entries) of x = 0 for this class
+  uint8_t size;       // class size
+  uint8_t tail_next;  // sum of sizes of deeper classes (tail[k+1])
+  uint8_t g;          // global class index (length / weight lookup)
+  uint8_t pad[3];
+};
+
+__host__ __device__ inline size_t al8(size_t x) { return (x + 7) & ~size_t(7); }
+
+// Per-warp shared memory layout (bytes).  K = max instance size, G = max
+// classes.  Tables hold sum_{d=1..K} (d + G) entries per array.
+struct Lay {
+  size_t a_tau, a_key, a_id, a_len;                         // input order
+  size_t o_tau, o_key, o_dnt, o_ws, o_dl, o_id, o_s, o_len; // tau order
+  size_t o_local, o_g, o_kr;
+  size_t c_len, c_w, c_start, c_cnt, c_list;                // classes
+  size_t sizes, ncls, lvl;                                  // per pool width d
+  size_t t_up, t_dn, t_tau;                                 // prefix tables
+  size_t ring_v, ring_p, ring_done, sol;
+  size_t total;
+  int T;
+};
+
+__host__ __device__ inline Lay make_lay(int K, int G, bool exact) {
+  Lay L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = al8(o + bytes); return r; };
+  L.a_tau = take(8 * K); L.a_key = take(8 * K); L.a_id = take(8 * K); L.a_len = take(4 * K);
+  L.o_tau = take(8 * K); L.o_key = take(8 * K); L.o_dnt = take(8 * K); L.o_ws = take(8 * K);
+  L.o_dl = take(8 * K); L.o_id = take(8 * K); L.o_s = take(4 * K); L.o_len = take(4 * K);
+  L.o_local = take(K); L.o_g = take(K); L.o_kr = take(K);
+  L.c_len = take(4 * G); L.c_w = take(8 * G); L.c_start = take(4 * (G + 1)); L.c_cnt = take(4 * G);
+  L.c_list = take(K);
+  L.sizes = take((size_t)K * G); L.ncls = take(K); L.lvl = take(8 * (size_t)K * G);
+  L.T = K * (K + 1) / 2 + K * G;
+  L.t_up = take(8 * (size_t)L.T); L.t_dn = take(8 * (size_t)L.T);
+  L.t_tau = exact ? take(8 * (size_t)L.T) : 0;
+  L.ring_v = take(8 * RING); L.ring_p = take(8 * RING); L.ring_done = take(RING);
+  L.sol = take(K);
+  L.total = o;
+  return L;
+}
+
+struct DftspArgs {
+  const eb_context* ctxs;
+  int n_ctx;
+  eb_search_params prm;
+  int64_t n_inst;
+  const int64_t* offsets;     // launch-local instance i -> absolute request rows
+  const int32_t* ctx_index;
+  int64_t req_base;           // absolute row of req arrays' element 0
+  eb_requests req;
+  int K, G;
+  size_t warp_bytes;
+  eb_dftsp_result out;        // per-instance arrays launch-local; solution at row - req_base
+  int64_t traj_base;          // absolute row of out.traj element 0
+  int* counter;
+};
+
+__device__ __forceinline__ int getV(uint64_t v0, uint64_t v1, int k) {
+  return (int)(((k < 8) ? (v0 >> (8 * k)) : (v1 >> (8 * (k - 8)))) & 0xff);
+}
+__device__ __forceinline__ void setV(uint64_t& v0, uint64_t& v1, int k, int x) {
+  if (k < 8) v0 = (v0 & ~(0xffULL << (8 * k))) | ((uint64_t)x << (8 * k));
+  else v1 = (v1 & ~(0xffULL << (8 * (k - 8)))) | ((uint64_t)x << (8 * (k - 8)));
+}
+
+// Inverse of the call numbering: calls for z = n, n-1, ..., each d = z..n.
+__device__ __forceinline__ void call_zd(int n, int c, int& z, int& d) {
+  int m = (int)((sqrtf(8.0f * (float)c + 1.0f) - 1.0f) * 0.5f);
+  while ((m + 1) * (m + 2) / 2 <= c) ++m;
+  while (m * (m + 1) / 2 > c) --m;
+  z = n - m;
+  d = z + (c - m * (m + 1) / 2);
+}
+
+// One dfs call's state (dftsp.py:157-182) with the per-level accumulator
+// arrays collapsed to the current level; the count stack val[] is packed
+// 8 bits per level into V0/V1.
+struct Lane {
+  int z, k, x, sel, ncl;
+  uint64_t V0, V1;
+  double acc_up, acc_dn, acc_lat, acc_tau;
+  int64_t acc_mem;
+  double k3z, slot_cap, lat_cap, mem_cap;
+  uint64_t vis, prn;
+};
+struct Tables {
+  const LevelInfo* row;   // levels of this partition
+  const double* up;       // prefix tables (entries at row[k].off + x)
+  const double* dn;
+  const double* tau;
+  const int32_t* len;     // by LevelInfo::g
+  const double* w;        // latency_weight by LevelInfo::g
+};
+
+// dfs entry (dftsp.py:161-182).  Returns 1 when the call ends at the root.
+template <bool PRUNE, bool INCL, bool EXACT>
+__device__ __forceinline__ int dfs_begin(Lane& s, const Tables& T, int z, int tail0, int ncl, double k3,
+                                         double slot_base, bool has_cap, double tau_min, double k2,
+                                         int64_t padded) {
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  s.z = z;
+  s.ncl = ncl;
+  s.k3z = mul(k3, i2d(z));                                   // k3z = coeff.k3 * z
+  s.slot_cap = has_cap ? sub(slot_base, s.k3z) : INF;        // slot_budget(z) feasibility.py:120-125
+  s.lat_cap = EXACT ? s.slot_cap : pymin(tau_min, s.slot_cap);  // dftsp.py:163
+  s.mem_cap = sub(k2, i2d(padded * (int64_t)z));             // mem_budget(z) feasibility.py:102-104
+  s.vis = 0; s.prn = 0;
+  if (PRUNE && tail0 < z) { s.prn = 1; return 1; }           // dftsp.py:166-167
+  s.vis = 1;
+  if (ncl == 0) return 1;                                    // dftsp.py:170-171
+  s.k = 0; s.sel = 0; s.V0 = s.V1 = 0;
+  s.acc_up = s.acc_dn = s.acc_lat = 0.0; s.acc_mem = 0; s.acc_tau = INF;
+  s.x = min(z, (int)T.row[0].size);                          // dftsp.py:182
+  return 0;
+}
+
+// One iteration of the dfs loop (dftsp.py:183-234): returns 0 (continue),
+// 1 (search exhausted, no solution) or 2 (leaf passed; counts in V0/V1
+// with val[k] = x).
+template <bool PRUNE, bool INCL, bool EXACT>
+__device__ __forceinline__ int dfs_step(Lane& s, const Tables& T) {
+  const LevelInfo li = T.row[s.k];
+  bool back = false;
+  bool skip = false;
+  if (PRUNE) {
+    int cap_below = li.tail_next + (INCL ? li.size : 0);     // dftsp.py:186
+    if (s.sel + s.x + cap_below < s.z) { s.prn += s.x + 1; skip = true; back = true; }
+  }
+  if (!skip) {
+    s.vis += 1;
+    int total = s.sel + s.x;
+    if (total == s.z) {                                      // leaf dftsp.py:193-210
+      double u = add(s.acc_up, T.up[li.off + s.x]);
+      double dl = add(s.acc_dn, T.dn[li.off + s.x]);
+      int64_t mem = s.acc_mem + (int64_t)s.x * T.len[li.g];
+      double lat = add(s.acc_lat, mul(i2d(s.x), T.w[li.g]));
+      double cap;
+      if (EXACT) {
+        double tau = (s.x == 0) ? s.acc_tau : pymin(s.acc_tau, T.tau[li.off + s.x]);
+        cap = pymin(sub(tau, s.k3z), s.slot_cap);
+      } else {
+        cap = s.lat_cap;
+      }
+      if (leq(u, 1.0) && leq(dl, 1.0) && leq(i2d(mem), s.mem_cap) && leq(lat, cap)) {
+        setV(s.V0, s.V1, s.k, s.x);
+        return 2;
+      }
+      if (s.x > 0) { s.x -= 1; return 0; }
+      back = true;
+    } else if (s.k == s.ncl - 1) {                           // dead end dftsp.py:211-214
+      s.vis += s.x;
+      back = true;
+    } else {                                                 // descend dftsp.py:215-226
+      setV(s.V0, s.V1, s.k, s.x);
+      s.acc_up = add(s.acc_up, T.up[li.off + s.x]);
+      s.acc_dn = add(s.acc_dn, T.dn[li.off + s.x]);
+      s.acc_mem += (int64_t)s.x * T.len[li.g];
+      s.acc_lat = add(s.acc_lat, mul(i2d(s.x), T.w[li.g]));
+      if (EXACT && s.x != 0) s.acc_tau = pymin(s.acc_tau, T.tau[li.off + s.x]);
+      s.sel = total;
+      s.k += 1;
+      s.x = min(s.z - total, (int)T.row[s.k].size);
+      return 0;
+    }
+  }
+  (void)back;
+  // backtrack dftsp.py:227-234
+  for (;;) {
+    if (s.k == 0) return 1;
+    s.k -= 1;
+    s.x = getV(s.V0, s.V1, s.k) - 1;
+    if (s.x >= 0) break;
+  }
+  // accumulators of level k = the same left fold over levels < k
+  s.sel = 0; s.acc_up = 0.0; s.acc_dn = 0.0; s.acc_lat = 0.0; s.acc_mem = 0;
+  s.acc_tau = __longlong_as_double(0x7ff0000000000000LL);
+  for (int j = 0; j < s.k; ++j) {
+    const LevelInfo lj = T.row[j];
+    int v = getV(s.V0, s.V1, j);
+    s.sel += v;
+    s.acc_up = add(s.acc_up, T.up[lj.off + v]);
+    s.acc_dn = add(s.acc_dn, T.dn[lj.off + v]);
+    s.acc_mem += (int64_t)v * T.len[lj.g];
+    s.acc_lat = add(s.acc_lat, mul(i2d(v), T.w[lj.g]));
+    if (EXACT && v != 0) s.acc_tau = pymin(s.acc_tau, T.tau[lj.off + v]);
+  }
+  return 0;
+}
+
+template <bool PRUNE, bool INCL, bool EXACT>
+__device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* smem) {
+  const int lane = threadIdx.x & 31;
+  const int K = A.K, G = A.G;
+  const Lay L = make_lay(K, G, EXACT);
+  double* a_tau = (double*)(smem + L.a_tau);
+  double* a_key = (double*)(smem + L.a_key);
+  int64_t* a_id = (int64_t*)(smem + L.a_id);
+  int32_t* a_len = (int32_t*)(smem + L.a_len);
+  double* o_tau = (double*)(smem + L.o_tau);
+  double* o_key = (double*)(smem + L.o_key);
+  double* o_dnt = (double*)(smem + L.o_dnt);
+  double* o_ws = (double*)(smem + L.o_ws);
+  double* o_dl = (double*)(smem + L.o_dl);
+  int64_t* o_id = (int64_t*)(smem + L.o_id);
+  int32_t* o_s = (int32_t*)(smem + L.o_s);
+  int32_t* o_len = (int32_t*)(smem + L.o_len);
+  uint8_t* o_local = smem + L.o_local;
+  uint8_t* o_g = smem + L.o_g;
+  uint8_t* o_kr = smem + L.o_kr;
+  int32_t* c_len = (int32_t*)(smem + L.c_len);
+  double* c_w = (double*)(smem + L.c_w);
+  int32_t* c_start = (int32_t*)(smem + L.c_start);
+  int32_t* c_cnt = (int32_t*)(smem + L.c_cnt);
+  uint8_t* c_list = smem + L.c_list;
+  uint8_t* sizes = smem + L.sizes;
+  uint8_t* ncls_d = smem + L.ncls;
+  LevelInfo* lvl = (LevelInfo*)(smem + L.lvl);
+  double* t_up = (double*)(smem + L.t_up);
+  double* t_dn = (double*)(smem + L.t_dn);
+  double* t_tau = EXACT ? (double*)(smem + L.t_tau) : nullptr;
+  uint64_t* ring_v = (uint64_t*)(smem + L.ring_v);
+  uint64_t* ring_p = (uint64_t*)(smem + L.ring_p);
+  uint8_t* ring_done = smem + L.ring_done;
+  uint8_t* sol = smem + L.sol;
+
+  const eb_dftsp_result& O = A.out;
+  const int64_t row0 = A.offsets[inst];
+  const int n = (int)(A.offsets[inst + 1] - row0);
+  const int64_t r0 = row0 - A.req_base;
+
+  auto put_status = [&](int st, int err) {
+    if (lane == 0) {
+      O.status[inst] = st;
+      if (O.error_index) O.error_index[inst] = err;
+      O.z_found[inst] = 0;
+      O.nodes_visited[inst] = 0;
+      O.nodes_pruned[inst] = 0;
+      if (O.n_classes) O.n_classes[inst] = 0;
+      if (O.traj_len) O.traj_len[inst] = 0;
+    }
+    if (O.metrics && lane < EB_N_METRICS) O.metrics[inst * EB_N_METRICS + lane] = 0.0;
+    if (lane < EB_MAX_CLASSES) {
+      if (O.counts) O.counts[inst * EB_MAX_CLASSES + lane] = 0;
+      if (O.class_lengths) O.class_lengths[inst * EB_MAX_CLASSES + lane] = 0;
+    }
+  };
+
+  int ci = A.ctx_index ? A.ctx_index[inst] : 0;
+  if (ci < 0 || ci >= A.n_ctx) { put_status(EB_ERR_INVALID_ARG, -1); return; }
+  if (n == 0) { put_status(EB_OK, -1); return; }     // dftsp.py:253-254
+  if (n > K || n > EB_MAX_K) { put_status(EB_ERR_K_TOO_LARGE, -1); return; }
+  const Ctx C = load_ctx(&A.ctxs[ci]);
+
+  // ---------------- setup: per request (lanes over i = lane, lane+32) -----
+  int s_i[2], len_i[2];
+  int64_t id_i[2];
+  double dl_i[2], w_i[2], g_i[2], p_i[2];
+  int padded = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int i = lane + 32 * h;
+    if (i < n) {
+      int64_t r = r0 + i;
+      s_i[h] = A.req.prompt_tokens[r];
+      len_i[h] = A.req.output_tokens[r];
+      id_i[h] = A.req.id[r];
+      dl_i[h] = A.req.deadline_s[r];
+      w_i[h] = A.req.waiting_s[r];
+      g_i[h] = A.req.channel_gain[r];
+      p_i[h] = A.req.uplink_power_w[r];
+      a_id[i] = id_i[h];
+      a_len[i] = len_i[h];
+      padded = max(padded, s_i[h]);
+    }
+  }
+  padded = __reduce_max_sync(EB_FULL, padded);             // dftsp.py:255
+  __syncwarp();
+  // Duplicate ids (coefficients are keyed by id, feasibility.py:164-166).
+  int err_dup = INT_MAX;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int i = lane + 32 * h;
+    if (i < n)
+      for (int j = 0; j < i; ++j)
+        if (a_id[j] == id_i[h]) { err_dup = min(err_dup, i); break; }
+  }
+  err_dup = __reduce_min_sync(EB_FULL, err_dup);
+  if (err_dup != INT_MAX) { put_status(EB_ERR_DUPLICATE_ID, err_dup); return; }
+
+  // derive_coefficients feasibility.py:133-167
+  const int64_t m1 = weight_bytes(C.m);
+  const double headroom = sub(div(C.M, C.alpha), i2d(m1));
+  if (headroom < 0) { put_status(EB_ERR_WEIGHTS_DO_NOT_FIT, -1); return; }
+  const int64_t kv = kv_per_token(C.m);
+  const int64_t gb = gen_base(C.m, padded);
+  const int64_t fi_pad = flops_initial(C.m, padded);
+  const double k2 = div(headroom, i2d(kv));
+  const double k3 = i2d(fi_pad - C.m.L * gb);
+  const double k4 = i2d(C.m.L * (gb - 2 * C.m.d));
+  const double k5 = i2d(2 * C.m.L * C.m.d);
+  const double slot_base = C.has_cap ? div(mul(C.cap_s, C.C), C.beta) : 0.0;  // feasibility.py:124
+
+  double key_i[2], dnt_i[2], tau_i[2];
+  int err_link = INT_MAX, err_code = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int i = lane + 32 * h;
+    key_i[h] = dnt_i[h] = tau_i[h] = 0.0;
+    if (i < n) {
+      double ku, kd;
+      int st = k_up_of(C, g_i[h], p_i[h], &ku);
+      if (!st) st = k_dn_of(C, g_i[h], &kd);
+      if (st) {
+        if (i < err_link) { err_link = i; err_code = st; }
+      } else {
+        key_i[h] = mul(i2d(s_i[h]), ku);       // min_uplink_fraction radio.py:94 (== k_up * s)
+        dnt_i[h] = mul(kd, i2d(len_i[h]));     // dftsp.py:127  k_down * n
+        tau_i[h] = tau_base_of(C, dl_i[h], w_i[h]);
+        a_tau[i] = tau_i[h];
+        a_key[i] = key_i[h];
+      }
+    }
+  }
+  {
+    int e = __reduce_min_sync(EB_FULL, err_link);
+    if (e != INT_MAX) {
+      int code = __shfl_sync(EB_FULL, err_code, e & 31);
+      // lane (e & 31) holds item e in slot h = e >> 5; err_code is that lane's min
+      put_status(code, e);
+      return;
+    }
+  }
+  __syncwarp();
+
+  // order = sorted by (-tau_base, id) (dftsp.py:257); classes by ascending
+  // output length with within-class order (key, id) (dftsp.py:71-82).
+  int t_i[2], gcls_i[2], kr_i[2];
+  bool first_i[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int i = lane + 32 * h;
+    t_i[h] = gcls_i[h] = kr_i[h] = 0;
+    first_i[h] = false;
+    if (i < n) {
+      int t = 0;
+      bool first = true;
+      for (int j = 0; j < n; ++j) {
+        double tj = a_tau[j];
+        t += (tj > tau_i[h]) || (tj == tau_i[h] && a_id[j] < id_i[h]);
+        if (j < i && a_len[j] == len_i[h]) first = false;
+      }
+      t_i[h] = t;
+      first_i[h] = first;
+    }
+  }
+  // class index = number of distinct lengths below mine
+  unsigned long long firstmask = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    unsigned b = __ballot_sync(EB_FULL, first_i[h]);
+    firstmask |= (unsigned long long)b << (32 * h);
+  }
+  const int Gi = __popcll(firstmask);
+  if (Gi > G || Gi > EB_MAX_CLASSES) { put_status(EB_ERR_TOO_MANY_CLASSES, -1); return; }
+  // Ladder check: the first off-ladder request in tau order (dftsp.py:63-70).
+  int bad_t = INT_MAX, bad_i = -1;
+  if (A.prm.ladder_len > 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int i = lane + 32 * h;
+      if (i < n) {
+        bool ok = false;
+        for (int q = 0; q < A.prm.ladder_len; ++q) ok |= (A.prm.ladder[q] == len_i[h]);
+        if (!ok && t_i[h] < bad_t) { bad_t = t_i[h]; bad_i = i; }
+      }
+    }
+  }
+  {
+    int bt = __reduce_min_sync(EB_FULL, bad_t);
+    if (bt != INT_MAX) {
+      unsigned who = __ballot_sync(EB_FULL, bad_t == bt);
+      int bi = __shfl_sync(EB_FULL, bad_i, __ffs(who) - 1);
+      put_status(EB_ERR_OFF_LADDER, bi);
+      return;
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int i = lane + 32 * h;
+    if (i < n) {
+      int g = 0, kr = 0;
+      for (int j = 0; j < n; ++j) {
+        bool fj = (firstmask >> j) & 1ULL;
+        g += fj && a_len[j] < len_i[h];
+        if (a_len[j] == len_i[h]) {
+          double kj = a_key[j];
+          kr += (kj < key_i[h]) || (kj == key_i[h] && a_id[j] < id_i[h]);
+        }
+      }
+      gcls_i[h] = g;
+      kr_i[h] = kr;
+      int t = t_i[h];
+      o_tau[t] = tau_i[h];
+      o_key[t] = key_i[h];
+      o_dnt[t] = dnt_i[h];
+      o_ws[t] = add(w_i[h], C.slots);   // r.waiting_s + slots (feasibility.py:222)
+      o_dl[t] = dl_i[h];
+      o_id[t] = id_i[h];
+      o_s[t] = s_i[h];
+      o_len[t] = len_i[h];
+      o_local[t] = (uint8_t)i;
+      o_g[t] = (uint8_t)g;
+      o_kr[t] = (uint8_t)kr;
+      if (first_i[h]) {
+        c_len[g] = len_i[h];
+        double fn = i2d(len_i[h]);
+        c_w[g] = add(mul(k4, fn), mul(mul(k5, fn), fn));   // latency_weight feasibility.py:108
+      }
+    }
+  }
+  if (lane < Gi) c_cnt[lane] = 0;
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int i = lane + 32 * h;
+    if (i < n) atomicAdd(&c_cnt[gcls_i[h]], 1);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    int acc = 0;
+    for (int g = 0; g < Gi; ++g) { c_start[g] = acc; acc += c_cnt[g]; }
+    c_start[Gi] = acc;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int i = lane + 32 * h;
+    if (i < n) c_list[c_start[gcls_i[h]] + kr_i[h]] = (uint8_t)t_i[h];
+  }
+  __syncwarp();
+
+  // ---------------- per pool width d: class sizes, levels, tables --------
+  const int nDG = n * Gi;
+  for (int w = lane; w < nDG; w += 32) {
+    int d = w / Gi + 1, g = w % Gi;
+    int cnt = 0, b = c_start[g], e = c_start[g + 1];
+    for (int q = b; q < e; ++q) cnt += c_list[q] < d;
+    sizes[(d - 1) * Gi + g] = (uint8_t)cnt;
+  }
+  __syncwarp();
+  for (int d = lane + 1; d <= n; d += 32) {
+    int base = (d - 1) * d / 2 + (d - 1) * Gi;
+    int k = 0, start = 0;
+    LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
+    for (int g = 0; g < Gi; ++g) {
+      int sz = sizes[(d - 1) * Gi + g];
+      if (sz > 0) {
+        LevelInfo li;
+        li.off = (uint16_t)(base + start);
+        li.size = (uint8_t)sz;
+        li.tail_next = 0;
+        li.g = (uint8_t)g;
+        li.pad[0] = li.pad[1] = li.pad[2] = 0;
+        row[k++] = li;
+      }
+      start += sz + 1;
+    }
+    ncls_d[d - 1] = (uint8_t)k;
+    int tail = 0;
+    for (int q = k - 1; q >= 0; --q) { row[q].tail_next = (uint8_t)tail; tail += row[q].size; }
+  }
+  for (int w = lane; w < nDG; w += 32) {
+    int d = w / Gi + 1, g = w % Gi;
+    int base = (d - 1) * d / 2 + (d - 1) * Gi;
+    int start = 0;
+    for (int g2 = 0; g2 < g; ++g2) start += sizes[(d - 1) * Gi + g2] + 1;
+    int off = base + start;
+    double cu = 0.0, cd = 0.0, tm = __longlong_as_double(0x7ff0000000000000LL);
+    t_up[off] = cu; t_dn[off] = cd;
+    if (EXACT) t_tau[off] = tm;
+    int x = 0, b = c_start[g], e = c_start[g + 1];
+    for (int q = b; q < e; ++q) {
+      int t = c_list[q];
+      if (t < d) {
+        ++x;
+        cu = add(cu, o_key[t]);                    // cu[-1] + k_up*s   (dftsp.py:126)
+        cd = add(cd, o_dnt[t]);                    // cd[-1] + k_down*n (dftsp.py:127)
+        t_up[off + x] = cu;
+        t_dn[off + x] = cd;
+        if (EXACT) { tm = pymin(tm, o_tau[t]); t_tau[off + x] = tm; }  // dftsp.py:128
+      }
+    }
+  }
+  if (lane < RING / 32 * 32) { ring_done[lane] = 0; ring_done[lane + 32] = 0; }
+  __syncwarp();
+
+  // ---------------- search: lanes = dfs calls in sequence order ----------
+  const int total_calls = n * (n + 1) / 2;
+  const bool collect = A.prm.collect_trajectory && O.traj && O.traj_offsets;
+  int64_t* traj = collect ? O.traj + 4 * (O.traj_offsets[inst] - A.traj_base) : nullptr;
+  int next_call = 0, best = INT_MAX, fold = 0;
+  uint64_t tot_v = 0, tot_p = 0;
+
+  Lane S;
+  S.z = S.k = S.x = S.sel = S.ncl = 0;
+  S.V0 = S.V1 = 0;
+  S.vis = S.prn = 0;
+  int c = -1, d = 0;
+  Tables T;
+  T.row = lvl; T.up = t_up; T.dn = t_dn; T.tau = t_tau; T.len = c_len; T.w = c_w;
+  int succ_c = INT_MAX, succ_k = 0, succ_d = 0, succ_z = 0;
+  uint64_t succ_V0 = 0, succ_V1 = 0;
+
+  auto finish_call = [&](int outcome) {
+    int slot = c % RING;
+    ring_v[slot] = S.vis; ring_p[slot] = S.prn; ring_done[slot] = 1;
+    if (traj) {
+      int64_t* tr = traj + 4 * (int64_t)c;
+      tr[0] = S.z; tr[1] = d; tr[2] = (int64_t)S.vis; tr[3] = (int64_t)S.prn;
+    }
+    if (outcome == 2) { succ_c = c; succ_k = S.k; succ_d = d; succ_z = S.z; succ_V0 = S.V0; succ_V1 = S.V1; }
+    c = -1;
+  };
+
+  for (;;) {
+    // 1. hand out calls to idle lanes (in sequence order, lowest lane first)
+    int limit = min(total_calls, best);
+    limit = min(limit, fold + RING);
+    unsigned want = __ballot_sync(EB_FULL, c < 0);
+    if (c < 0) {
+      int my = next_call + __popc(want & lanemask_lt());
+      if (my < limit) {
+        c = my;
+        int z;
+        call_zd(n, c, z, d);
+        T.row = lvl + (size_t)(d - 1) * Gi;
+        double tau_min = sub(o_tau[d - 1], mul(k3, i2d(z)));       // bases[d-1] - k3*z (dftsp.py:267)
+        if (dfs_begin<PRUNE, INCL, EXACT>(S, T, z, d, ncls_d[d - 1], k3, slot_base, C.has_cap, tau_min, k2,
+                                          padded))
+          finish_call(1);
+      }
+    }
+    next_call += max(0, min(__popc(want), limit - next_call));
+
+    // 2. one node of each running call
+    if (c >= 0) {
+      int outcome = dfs_step<PRUNE, INCL, EXACT>(S, T);
+      if (outcome) finish_call(outcome);
+    }
+
+    // 3. first success in sequence order; abort speculative calls behind it
+    best = __reduce_min_sync(EB_FULL, succ_c);
+    if (c > best) c = -1;
+    __syncwarp();
+    // 4. fold completed calls in sequence order (uniform across the warp)
+    for (;;) {
+      int lim = (best == INT_MAX) ? total_calls : best + 1;
+      if (fold >= lim || fold >= next_call) break;
+      int slot = fold % RING;
+      if (!ring_done[slot]) break;
+      tot_v += ring_v[slot];
+      tot_p += ring_p[slot];
+      ++fold;
+      __syncwarp();
+      if (lane == 0) ring_done[slot] = 0;
+      __syncwarp();
+    }
+    if (best != INT_MAX ? fold > best : fold >= total_calls) break;
+  }
+
+  // ---------------- finish ------------------------------------------------
+  const bool found = best != INT_MAX;
+  int zf = 0, dwin = 0, kwin = 0;
+  uint64_t W0 = 0, W1 = 0;
+  if (found) {
+    unsigned who = __ballot_sync(EB_FULL, succ_c == best);
+    int src = __ffs(who) - 1;
+    zf = __shfl_sync(EB_FULL, succ_z, src);
+    dwin = __shfl_sync(EB_FULL, succ_d, src);
+    kwin = __shfl_sync(EB_FULL, succ_k, src);
+    W0 = __shfl_sync(EB_FULL, succ_V0, src);
+    W1 = __shfl_sync(EB_FULL, succ_V1, src);
+  }
+  int status = EB_OK;
+  double met[EB_N_METRICS];
+#pragma unroll
+  for (int q = 0; q < EB_N_METRICS; ++q) met[q] = 0.0;
+  met[EB_MET_PADDED] = (double)padded;
+  const LevelInfo* wrow = lvl + (size_t)(dwin > 0 ? dwin - 1 : 0) * Gi;
+  const int wncls = found ? ncls_d[dwin - 1] : 0;
+  if (found) {
+    // recover_subset (dftsp.py:85-93) in recover order, then check_direct
+    // (feasibility.py:192-223) exactly as dftsp.py:276 calls it.
+    if (lane == 0) {
+      int q = 0;
+      for (int kk = 0; kk < wncls; ++kk) {
+        int cnt = (kk <= kwin) ? getV(W0, W1, kk) : 0;
+        int g = wrow[kk].g;
+        int taken = 0;
+        for (int p = c_start[g]; p < c_start[g + 1] && taken < cnt; ++p) {
+          int t = c_list[p];
+          if (t < dwin) { sol[q++] = (uint8_t)t; ++taken; }
+        }
+      }
+      double up = 0.0, dn = 0.0;
+      int64_t sn = 0, fl_pool = 0, fl_batch = 0;
+      int pb = 0;
+      for (int j = 0; j < zf; ++j) {
+        int t = sol[j];
+        up = add(up, o_key[t]);      // r.prompt_tokens * k_up
+        dn = add(dn, o_dnt[t]);      // r.output_tokens * k_down
+        sn += o_len[t];
+        pb = max(pb, o_s[t]);
+      }
+      int64_t mem = m1 + kv * (int64_t)padded * zf;
+      mem += kv * sn;
+      fl_pool = (int64_t)zf * fi_pad;
+      for (int j = 0; j < zf; ++j) fl_pool += flops_autoregressive(C.m, padded, o_len[sol[j]]);
+      double compute_s = compute_seconds(C, fl_pool);
+      bool ok = leq(up, 1.0) && leq(dn, 1.0) && leq(mul(C.alpha, i2d(mem)), C.M);
+      if (ok && C.has_cap) ok = leq(compute_s, C.cap_s);
+      for (int j = 0; ok && j < zf; ++j) ok = leq(add(o_ws[sol[j]], compute_s), o_dl[sol[j]]);
+      if (!ok) status = EB_ERR_REVERIFY;
+      // batch_cost at the batch's own padding (sim.py:372-376)
+      int64_t mem_b = m1 + kv * (int64_t)pb * zf + kv * sn;
+      fl_batch = (int64_t)zf * flops_initial(C.m, pb);
+      for (int j = 0; j < zf; ++j) fl_batch += flops_autoregressive(C.m, pb, o_len[sol[j]]);
+      met[EB_MET_UP_SUM] = up;
+      met[EB_MET_DN_SUM] = dn;
+      met[EB_MET_MEM_POOLPAD] = mul(C.alpha, i2d(mem));
+      met[EB_MET_LAT_POOLPAD] = compute_s;
+      met[EB_MET_MEM_BATCHPAD] = mul(C.alpha, i2d(mem_b));
+      met[EB_MET_LAT_BATCHPAD] = compute_seconds(C, fl_batch);
+      met[EB_MET_WIN_D] = (double)dwin;
+    }
+    status = __shfl_sync(EB_FULL, status, 0);
+    __syncwarp();
+    // solution sorted by request id (dftsp.py:281)
+    if (status == EB_OK && O.solution) {
+      for (int j = lane; j < zf; j += 32) {
+        int t = sol[j];
+        int64_t idv = o_id[t];
+        int rank = 0;
+        for (int q = 0; q < zf; ++q) rank += o_id[sol[q]] < idv;
+        O.solution[r0 + rank] = o_local[t];
+      }
+    }
+  }
+  if (lane == 0) {
+    O.status[inst] = status;
+    if (O.error_index) O.error_index[inst] = -1;
+    O.z_found[inst] = (found && status == EB_OK) ? zf : 0;
+    O.nodes_visited[inst] = (int64_t)tot_v;
+    O.nodes_pruned[inst] = (int64_t)tot_p;
+    if (O.n_classes) O.n_classes[inst] = (found && status == EB_OK) ? wncls : 0;
+    if (O.traj_len) O.traj_len[inst] = found ? best + 1 : total_calls;
+    if (O.metrics)
+      for (int q = 0; q < EB_N_METRICS; ++q) O.metrics[inst * EB_N_METRICS + q] = met[q];
+  }
+  if (lane < EB_MAX_CLASSES) {
+    bool live = found && status == EB_OK && lane < wncls;
+    int cnt = 0, clen = 0;
+    if (live) {
+      cnt = (lane <= kwin) ? getV(W0, W1, lane) : 0;
+      clen = c_len[wrow[lane].g];
+    }
+    if (O.counts) O.counts[inst * EB_MAX_CLASSES + lane] = cnt;
+    if (O.class_lengths) O.class_lengths[inst * EB_MAX_CLASSES + lane] = clen;
+  }
+}
+
+template <bool PRUNE, bool INCL, bool EXACT>
+__global__ void __launch_bounds__(128) dftsp_kernel(DftspArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_all[];
+  const int warp = threadIdx.x >> 5;
+  unsigned char* smem = smem_all + warp * A.warp_bytes;
+  for (;;) {
+    int64_t inst = 0;
+    if ((threadIdx.x & 31) == 0) inst = atomicAdd(A.counter, 1);
+    inst = __shfl_sync(EB_FULL, inst, 0);
+    if (inst >= A.n_inst) break;
+    solve_instance<PRUNE, INCL, EXACT>(A, inst, smem);
+    __syncwarp();
+  }
+}
+
+
+// Single dfs() call on a caller-built partition (dfs(z, part, coeff, tau_min)
+// dftsp.py:135-234): builds SearchTables (dftsp.py:110-132) in shared memory
+// and runs the same dfs_begin/dfs_step as the batched search.
+template <bool PRUNE, bool INCL, bool EXACT>
+__global__ void dfs_single_kernel(int z, int ncls, const int32_t* sizes, const int32_t* lengths,
+                                  const int32_t* prompt, const double* k_up, const double* k_dn,
+                                  const double* deadline, const double* waiting, const double* co,
+                                  int64_t padded, int has_tau, double tau_min, int32_t* res) {
+  __shared__ LevelInfo row[EB_MAX_CLASSES];
+  __shared__ double up[EB_MAX_K + EB_MAX_CLASSES], dn[EB_MAX_K + EB_MAX_CLASSES],
+      tau[EB_MAX_K + EB_MAX_CLASSES], w[EB_MAX_CLASSES];
+  __shared__ int32_t len[EB_MAX_CLASSES];
+  if (threadIdx.x != 0) return;
+  const double k2 = co[0], k3 = co[1], k4 = co[2], k5 = co[3], sb = co[4];
+  const double slots = co[5], Cf = co[6], beta = co[7];
+  int off = 0, m = 0, tail0 = 0;
+  for (int k = 0; k < ncls; ++k) tail0 += sizes[k];
+  int tail = tail0;
+  for (int k = 0; k < ncls; ++k) {
+    int sz = sizes[k];
+    tail -= sz;
+    row[k].off = (uint16_t)off; row[k].size = (uint8_t)sz; row[k].tail_next = (uint8_t)tail;
+    row[k].g = (uint8_t)k; row[k].pad[0] = row[k].pad[1] = row[k].pad[2] = 0;
+    len[k] = lengths[k];
+    double fn = i2d(lengths[k]);
+    w[k] = add(mul(k4, fn), mul(mul(k5, fn), fn));              // latency_weight
+    double cu = 0.0, cd = 0.0, tm = __longlong_as_double(0x7ff0000000000000LL);
+    up[off] = cu; dn[off] = cd; tau[off] = tm;
+    for (int q = 0; q < sz; ++q, ++m) {
+      cu = add(cu, mul(k_up[m], i2d(prompt[m])));             // cu[-1] + k_up * s     (dftsp.py:126)
+      cd = add(cd, mul(k_dn[m], fn));                          // cd[-1] + k_down * n   (dftsp.py:127)
+      double tb = div(mul(sub(sub(deadline[m], waiting[m]), slots), Cf), beta);  // tau_base :110-114
+      tm = pymin(tm, tb);
+      up[off + q + 1] = cu; dn[off + q + 1] = cd; tau[off + q + 1] = tm;
+    }
+    off += sz + 1;
+  }
+  Tables T;
+  T.row = row; T.up = up; T.dn = dn; T.tau = tau; T.len = len; T.w = w;
+  Lane s;
+  s.k = 0; s.V0 = s.V1 = 0;
+  const bool has_cap = sb == sb;   // NaN marks slot_cap_s None
+  int r = dfs_begin<PRUNE, INCL, EXACT>(s, T, z, tail0, ncls, k3, has_cap ? sb : 0.0, has_cap,
+                                        has_tau ? tau_min : 0.0, k2, padded);
+  while (r == 0) r = dfs_step<PRUNE, INCL, EXACT>(s, T);
+  res[0] = (r == 2);
+  res[1] = (r == 2) ? s.k : -1;
+  for (int k = 0; k < EB_MAX_CLASSES; ++k) res[2 + k] = (r == 2 && k < ncls && k <= s.k) ? getV(s.V0, s.V1, k) : 0;
+  int64_t v = (int64_t)s.vis, p = (int64_t)s.prn;
+  *(int64_t*)(res + 2 + EB_MAX_CLASSES) = v;
+  *(int64_t*)(res + 2 + EB_MAX_CLASSES + 2) = p;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Host-side launcher (device pointers, caller's stream).
+// ---------------------------------------------------------------------------
+size_t dftsp_warp_bytes(int K, int G, bool exact) { return make_lay(K, G, exact).total; }
+
+int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_ctx,
+                 const eb_search_params& prm, int64_t n_inst, const int64_t* d_off,
+                 const int32_t* d_ctx_index, int64_t req_base, const eb_requests& d_req,
+                 int K, const eb_dftsp_result& d_out, int64_t traj_base, int* d_counter) {
+  if (n_inst <= 0) return EB_OK;
+  int G = prm.ladder_len > 0 ? prm.ladder_len : (K < EB_MAX_CLASSES ? K : EB_MAX_CLASSES);
+  if (G < 1) G = 1;
+  const bool exact = prm.exact_tau != 0;
+  DftspArgs A;
+  A.ctxs = d_ctxs; A.n_ctx = n_ctx; A.prm = prm; A.n_inst = n_inst; A.offsets = d_off;
+  A.ctx_index = d_ctx_index; A.req_base = req_base; A.req = d_req; A.K = K; A.G = G;
+  A.warp_bytes = al8(dftsp_warp_bytes(K, G, exact));
+  A.out = d_out; A.traj_base = traj_base; A.counter = d_counter;
+  const int warps = 4;
+  size_t smem = A.warp_bytes * warps;
+  if (smem > 227 * 1024) { set_error("instance size K=%d needs %zu B shared memory per block", K, smem); return EB_ERR_K_TOO_LARGE; }
+  void (*kern)(DftspArgs);
+  const bool P = prm.pruning != 0, I = prm.inclusive_bound != 0;
+  if (P) {
+    if (I) kern = exact ? dftsp_kernel<true, true, true> : dftsp_kernel<true, true, false>;
+    else kern = exact ? dftsp_kernel<true, false, true> : dftsp_kernel<true, false, false>;
+  } else {
+    if (I) kern = exact ? dftsp_kernel<false, true, true> : dftsp_kernel<false, true, false>;
+    else kern = exact ? dftsp_kernel<false, false, true> : dftsp_kernel<false, false, false>;
+  }
+  EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));
+  if (per_sm < 1) per_sm = 1;
+  int64_t want = (n_inst + warps - 1) / warps;
+  int64_t grid = (int64_t)per_sm * h->num_sms;
+  if (grid > want) grid = want;
+  EB_CUDA(cudaMemsetAsync(d_counter, 0, sizeof(int), st));
+  kern<<<(unsigned)grid, 32 * warps, smem, st>>>(A);
+  EB_CUDA(cudaGetLastError());
+  h->launches += 1;
+  return EB_OK;
+}
+
+int launch_dfs_single(eb_handle* h, cudaStream_t st, int z, int ncls, const int32_t* sizes,
+                      const int32_t* lengths, const int32_t* prompt, const double* ku, const double* kd,
+                      const double* dl, const double* wt, const double* co, int64_t padded, int has_tau,
+                      double tau_min, const eb_search_params& prm, int32_t* res) {
+  void (*kern)(int, int, const int32_t*, const int32_t*, const int32_t*, const double*, const double*,
+               const double*, const double*, const double*, int64_t, int, double, int32_t*);
+  const bool P = prm.pruning != 0, I = prm.inclusive_bound != 0, E = prm.exact_tau != 0;
+  if (P) {
+    if (I) kern = E ? dfs_single_kernel<true, true, true> : dfs_single_kernel<true, true, false>;
+    else kern = E ? dfs_single_kernel<true, false, true> : dfs_single_kernel<true, false, false>;
+  } else {
+    if (I) kern = E ? dfs_single_kernel<false, true, true> : dfs_single_kernel<false, true, false>;
+    else kern = E ? dfs_single_kernel<false, false, true> : dfs_single_kernel<false, false, false>;
+  }
+  kern<<<1, 32, 0, st>>>(z, ncls, sizes, lengths, prompt, ku, kd, dl, wt, co, padded, has_tau, tau_min, res);
+  EB_CUDA(cudaGetLastError());
+  h->launches += 1;
+  return EB_OK;
+}
+
+}  // namespace eb

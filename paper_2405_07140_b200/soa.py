@@ -1,0 +1,154 @@
+"""Structure-of-arrays packing between reference-style objects and the C ABI.
+
+Host logic only (no arithmetic of the hot path): flattens ``EdgeContext``-like
+objects into ``eb_context`` records and ``Request``-like objects into SoA
+columns, and wraps batches of instances (CSR offsets) for the batched entry
+points.  Objects are duck-typed, so the reference's own ``edgebatch``
+dataclasses can be passed unchanged.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import CTX_DTYPE, eb_batch, eb_requests, ptr
+
+REQ_FIELDS = (("id", np.int64), ("prompt_tokens", np.int32), ("output_tokens", np.int32),
+              ("deadline_s", np.float64), ("waiting_s", np.float64), ("tolerance", np.float64),
+              ("channel_gain", np.float64), ("uplink_power_w", np.float64))
+INT32_MAX = 2**31 - 1
+
+
+def _int_field(value, name: str) -> int:
+    iv = int(value)
+    if iv != value:
+        raise ValueError(f"{name} must be integral for the device cost model, got {value!r}")
+    return iv
+
+
+def context_record(ctx, delta: float = 0.0) -> np.ndarray:
+    """One eb_context record from an EdgeContext-like object (feasibility.py:59-71)."""
+    rec = np.zeros(1, dtype=CTX_DTYPE)
+    llm, quant, radio, node = ctx.llm, ctx.quant, ctx.radio, ctx.node
+    rec["layers"] = llm.layers
+    rec["hidden_dim"] = llm.hidden_dim
+    rec["head_count"] = llm.head_count
+    rec["head_dim"] = llm.head_dim
+    rec["ffn_dim"] = llm.ffn_dim
+    rec["bytes_per_param"] = llm.bytes_per_param
+    rec["alpha"] = float(quant.alpha)
+    rec["beta"] = float(quant.beta)
+    rec["delta_ppl"] = float(delta)
+    rec["uplink_band_hz"] = float(radio.uplink_band_hz)
+    rec["downlink_band_hz"] = float(radio.downlink_band_hz)
+    rec["downlink_power_w"] = float(radio.downlink_power_w)
+    rec["noise_density_w_hz"] = float(radio.noise_density_w_hz)
+    rec["uplink_slot_s"] = float(radio.uplink_slot_s)
+    rec["downlink_slot_s"] = float(radio.downlink_slot_s)
+    rec["bits_per_token"] = _int_field(radio.bits_per_token, "bits_per_token")
+    rec["flops_per_s"] = float(node.flops_per_s)
+    rec["memory_bytes"] = float(node.memory_bytes)
+    rec["gpu_count"] = int(node.gpu_count)
+    cap = getattr(ctx, "slot_cap_s", None)
+    rec["has_slot_cap"] = 0 if cap is None else 1
+    rec["slot_cap_s"] = 0.0 if cap is None else float(cap)
+    return rec
+
+
+def request_columns(reqs) -> dict:
+    """SoA columns of a list of Request-like objects (order preserved)."""
+    n = len(reqs)
+    cols = {name: np.empty(n, dtype=dt) for name, dt in REQ_FIELDS}
+    for j, r in enumerate(reqs):
+        s, o = int(r.prompt_tokens), int(r.output_tokens)
+        if not (0 <= s <= INT32_MAX and 0 <= o <= INT32_MAX):
+            raise ValueError("prompt/output token counts must fit in int32 for the device path")
+        cols["id"][j] = r.id
+        cols["prompt_tokens"][j] = s
+        cols["output_tokens"][j] = o
+        cols["deadline_s"][j] = r.deadline_s
+        cols["waiting_s"][j] = r.waiting_s
+        cols["tolerance"][j] = r.tolerance
+        cols["channel_gain"][j] = r.link.channel_gain
+        cols["uplink_power_w"][j] = r.link.uplink_power_w
+    return cols
+
+
+def requests_struct(cols: dict) -> eb_requests:
+    s = eb_requests()
+    for name, _ in REQ_FIELDS:
+        a = cols.get(name)
+        setattr(s, name, ptr(a) if a is not None else None)
+    return s
+
+
+@dataclass
+class InstanceBatch:
+    """A batch of independent instances: CSR offsets over SoA request columns.
+
+    Columns are numpy arrays (host) or torch tensors (device, then
+    ``on_device`` is True).  ``contexts`` is an array of eb_context records;
+    ``ctx_index`` maps each instance to one of them.
+    """
+
+    offsets: object
+    columns: dict
+    contexts: np.ndarray
+    ctx_index: object = None
+    k_max: int = 0
+    on_device: bool = False
+
+    @property
+    def n_inst(self) -> int:
+        return int(self.offsets.shape[0]) - 1
+
+    @property
+    def n_req(self) -> int:
+        return int(self.columns["prompt_tokens"].shape[0])
+
+    def struct(self) -> eb_batch:
+        b = eb_batch()
+        b.n_inst = self.n_inst
+        b.n_req = self.n_req
+        b.offsets = ptr(self.offsets)
+        b.ctx_index = ptr(self.ctx_index)
+        b.req = requests_struct(self.columns)
+        b.k_max = int(self.k_max)
+        return b
+
+    def contexts_ptr(self):
+        return C.c_void_p(self.contexts.ctypes.data)
+
+    @classmethod
+    def from_pools(cls, pools, contexts, ctx_index=None) -> "InstanceBatch":
+        """Pack lists of Request-like objects (one list per instance)."""
+        sizes = [len(p) for p in pools]
+        offsets = np.zeros(len(pools) + 1, dtype=np.int64)
+        np.cumsum(sizes, out=offsets[1:])
+        flat = [r for p in pools for r in p]
+        cols = request_columns(flat)
+        if not isinstance(contexts, np.ndarray):
+            contexts = np.concatenate([context_record(c) for c in contexts])
+        ci = None if ctx_index is None else np.ascontiguousarray(ctx_index, dtype=np.int32)
+        return cls(offsets, cols, contexts, ci, max(sizes) if sizes else 1)
+
+
+def search_params(pruning=True, inclusive_bound=False, exact_tau=False, collect_trajectory=False, ladder=None):
+    p = _lib.eb_search_params()
+    p.pruning = int(bool(pruning))
+    p.inclusive_bound = int(bool(inclusive_bound))
+    p.exact_tau = int(bool(exact_tau))
+    p.collect_trajectory = int(bool(collect_trajectory))
+    if ladder is None:
+        p.ladder_len = 0
+    else:
+        vals = sorted(set(int(v) for v in ladder))
+        if len(vals) > _lib.EB_MAX_CLASSES:
+            raise ValueError(f"ladder has {len(vals)} classes; the device supports {_lib.EB_MAX_CLASSES}")
+        p.ladder_len = len(vals)
+        for i, v in enumerate(vals):
+            p.ladder[i] = v
+    return p

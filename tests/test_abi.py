@@ -1,0 +1,72 @@
+"""The C-ABI library builds, loads without a GPU and exports exactly the
+entry points include/edgebatch_b200.h declares; ctypes layouts match C."""
+import ctypes
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from helpers import ROOT
+from paper_2405_07140_b200 import _lib
+from paper_2405_07140_b200._build import build_library
+
+HEADER = os.path.join(ROOT, "include", "edgebatch_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int32_t|int64_t|const char \*)\s*(eb_[a-z_0-9]+)\s*\(", text, re.M)))
+
+
+def test_library_builds_and_loads():
+    path = build_library()
+    assert os.path.exists(path)
+    lib = _lib.load()
+    assert lib.eb_abi_version() == 1
+    assert lib.eb_status_string(0) == b"ok"
+
+
+def test_every_declared_symbol_is_exported():
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    lib = ctypes.CDLL(build_library())
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.EXPORTED_SYMBOLS), set(syms) ^ set(_lib.EXPORTED_SYMBOLS)
+
+
+def test_cubin_targets_sm100a():
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump):
+        pytest.skip("cuobjdump missing")
+    out = subprocess.run([cuobjdump, "--list-elf", build_library()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_struct_layouts_match_c(tmp_path):
+    gcc = shutil.which("gcc")
+    if not gcc:
+        pytest.skip("gcc missing")
+    src = tmp_path / "lay.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "edgebatch_b200.h"\n'
+                   'int main(){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(eb_context), sizeof(eb_requests),'
+                   ' sizeof(eb_batch), sizeof(eb_search_params), sizeof(eb_dftsp_result),'
+                   ' offsetof(eb_batch, k_max));return 0;}\n')
+    exe = tmp_path / "lay"
+    subprocess.run([gcc, "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
+    want = [ctypes.sizeof(_lib.eb_context), ctypes.sizeof(_lib.eb_requests), ctypes.sizeof(_lib.eb_batch),
+            ctypes.sizeof(_lib.eb_search_params), ctypes.sizeof(_lib.eb_dftsp_result),
+            _lib.eb_batch.k_max.offset]
+    assert got == want
+
+
+def test_no_gpu_means_loud_failure():
+    """Without a device the product raises -- there is no CPU fallback."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(_lib.EdgebatchNativeError):
+        _lib.Handle(0)

@@ -1,0 +1,120 @@
+"""K3 (instance-parallel DFTSP) parity on the GPU: bit-exact solution ids,
+counts, z, nodes_visited and nodes_pruned against (a) golden fixtures from the
+reference itself and (b) the C oracle on fresh seeded corpora."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from gen_random import group_by_ladder, random_batch
+from helpers import ALL_CORPORA, FLAGS, compare_corpus, corpus_path, groups, load_corpus, sub_batch
+from paper_2405_07140_b200 import search
+
+pytestmark = pytest.mark.gpu
+
+RES_KEYS = ("status", "z_found", "nodes_visited", "nodes_pruned", "n_classes", "counts", "class_lengths")
+
+
+def _gpu_solve(batch, ladder=None, **flags):
+    return search.solve_batch(batch, ladder=ladder, **flags)
+
+
+@pytest.mark.parametrize("name", ALL_CORPORA)
+def test_gpu_matches_reference_goldens(name):
+    if not os.path.exists(corpus_path(name)):
+        pytest.skip("corpus missing")
+    d = load_corpus(name)
+    tags = [t for t in FLAGS if f"{t}_z" in d]
+    for tag in tags:
+        bad = compare_corpus(d, tag, _gpu_solve, use_ladder=(tag != "NL"))
+        assert not bad, f"{name}/{tag}: {bad[:3]}"
+
+
+def _assert_same(dev, orc, batch, what):
+    for k in RES_KEYS:
+        a, b = getattr(dev, k), orc[k]
+        if not np.array_equal(a, b):
+            i = int(np.nonzero((a != b).reshape(len(a), -1).any(axis=1))[0][0])
+            raise AssertionError(f"{what}: {k} differs at instance {i}: gpu={a[i]} oracle={b[i]}")
+    ok = dev.status == 0
+    for i in np.nonzero(ok)[0]:
+        lo = int(batch.offsets[i])
+        z = int(dev.z_found[i])
+        assert np.array_equal(dev.solution[lo:lo + z], orc["solution"][lo:lo + z]), f"{what}: solution {i}"
+        assert np.array_equal(dev.metrics[i], orc["metrics"][i]), f"{what}: metrics {i}"
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+@pytest.mark.parametrize("tag", ["P", "NP", "PI", "PE"])
+def test_gpu_matches_oracle_fresh_corpora(seed, tag):
+    batch, ladders = random_batch(1000 * seed + hash(tag) % 97, 600)
+    for lad, (idx, sb) in group_by_ladder(batch, ladders).items():
+        dev = search.solve_batch(sb, ladder=lad, **FLAGS[tag])
+        orc = oracle.dftsp_batch(sb, ladder=lad, threads=8, **FLAGS[tag])
+        _assert_same(dev, orc, sb, f"seed {seed} {tag} ladder {lad}")
+
+
+def test_gpu_matches_oracle_no_ladder_many_classes():
+    batch, _ = random_batch(77, 400, k_max=20, max_classes=5)
+    dev = search.solve_batch(batch, ladder=None)
+    orc = oracle.dftsp_batch(batch, ladder=None, threads=8)
+    _assert_same(dev, orc, batch, "no ladder, <=5 classes")
+
+
+def test_gpu_large_k_and_trajectory():
+    batch, ladders = random_batch(5, 120, k_min=30, k_max=48, max_classes=4)
+    for lad, (idx, sb) in group_by_ladder(batch, ladders).items():
+        dev = search.solve_batch(sb, ladder=lad, collect_trajectory=True)
+        orc = oracle.dftsp_batch(sb, ladder=lad, collect_trajectory=True, threads=8)
+        _assert_same(dev, orc, sb, f"K 30-48 ladder {lad}")
+        assert np.array_equal(dev.traj_len, orc["traj_len"])
+        for j in range(sb.n_inst):
+            t0 = int(dev.traj_offsets[j])
+            n = int(dev.traj_len[j])
+            assert np.array_equal(dev.traj[t0:t0 + n], orc["traj"][t0:t0 + n]), j
+
+
+def test_gpu_trajectory_matches_reference():
+    d = load_corpus("random_34")
+    lens = d["P_traj_len"]
+    starts = np.concatenate([[0], np.cumsum(lens)])
+    for ladder, ids in groups(d).items():
+        b = sub_batch(d, ids)
+        res = search.solve_batch(b, ladder=ladder, collect_trajectory=True)
+        for j, i in enumerate(ids):
+            t0 = int(res.traj_offsets[j])
+            got = res.traj[t0:t0 + int(res.traj_len[j])]
+            assert np.array_equal(got, d["P_traj"][starts[i]:starts[i + 1]]), i
+
+
+def test_gpu_k64_and_sixteen_classes():
+    """Device limits: 64 candidates, 16 output classes (no ladder)."""
+    batch, _ = random_batch(99, 6, k_min=64, k_max=64, max_classes=5)
+    # spread outputs over 16 distinct lengths
+    rng = np.random.default_rng(1)
+    batch.columns["output_tokens"][:] = rng.choice(np.arange(1, 17) * 8, size=batch.n_req)
+    dev = search.solve_batch(batch, ladder=None)
+    orc = oracle.dftsp_batch(batch, ladder=None, threads=6)
+    _assert_same(dev, orc, batch, "K=64, 16 classes")
+
+
+def test_gpu_edge_statuses():
+    """Empty pools, duplicate ids, off-ladder, weights-do-not-fit: same status
+    and offending index as the oracle."""
+    batch, ladders = random_batch(3, 64, k_min=0, k_max=6)
+    b = batch
+    # duplicate ids in instance 5, off-ladder output in instance 7, tiny memory in instance 9
+    lo5 = int(b.offsets[5])
+    if b.offsets[6] - lo5 >= 2:
+        b.columns["id"][lo5 + 1] = b.columns["id"][lo5]
+    lo7 = int(b.offsets[7])
+    if b.offsets[8] > lo7:
+        b.columns["output_tokens"][lo7] = 999
+    b.contexts[9]["memory_bytes"] = 1.0
+    lad = (16, 32, 64, 128, 256)
+    dev = search.solve_batch(b, ladder=lad)
+    orc = oracle.dftsp_batch(b, ladder=lad)
+    assert np.array_equal(dev.status, orc["status"])
+    assert np.array_equal(dev.error_index, orc["error_index"])
+    _assert_same(dev, orc, b, "edge statuses")
