@@ -56,6 +56,8 @@ def load():
         lib.oracle_work_reset.argtypes = []
         lib.oracle_work_get.restype = None
         lib.oracle_work_get.argtypes = [P]
+        lib.oracle_exhaustive_level.restype = I64
+        lib.oracle_exhaustive_level.argtypes = [P, I32, P, P, P, P, P, P, P, I32, I64, I64]
         lib.oracle_nob.restype = None
         lib.oracle_nob.argtypes = [P, I32, P, P, P, F64, F64, I32, P, P, P, P]
         _o = lib
@@ -119,3 +121,21 @@ def work_counters(batch: InstanceBatch, ladder=None, threads=1, **flags) -> dict
     w = np.zeros(4, np.int64)
     lib.oracle_work_get(w.ctypes.data)
     return dict(leaf_checks=int(w[0]), descends=int(w[1]), prune_events=int(w[2]))
+
+
+def level_evaluator(ctx_rec, cols):
+    """CPU twin of brute.device_level_range: (z, lo, hi) -> first feasible rank or -1."""
+    lib = load()
+    a = {k: np.ascontiguousarray(v) for k, v in cols.items()}
+    n = int(a["prompt_tokens"].shape[0])
+
+    def level(z, lo, hi):
+        r = lib.oracle_exhaustive_level(ctx_rec.ctypes.data, n, a["id"].ctypes.data, a["prompt_tokens"].ctypes.data,
+                                        a["output_tokens"].ctypes.data, a["deadline_s"].ctypes.data,
+                                        a["waiting_s"].ctypes.data, a["channel_gain"].ctypes.data,
+                                        a["uplink_power_w"].ctypes.data, int(z), int(lo), int(hi))
+        if r == -2:
+            raise ValueError("spectral efficiency is zero")
+        return int(r)
+
+    return level

@@ -1,0 +1,145 @@
+"""Brute-force 2^K search sharded across GPUs by subset rank (config 4).
+
+``exhaustive_optimal(mode="subsets")`` (reference dftsp.py:305-313) returns the
+first feasible subset in itertools.combinations order, searching sizes from K
+down.  Equivalently: z* = the largest size with any
+feasible subset and r* = the smallest lexicographic rank among feasible
+subsets of size z*; nodes_visited = sum_{z > z*} C(K, z) + r* + 1.
+
+Sharding: every level's rank range [0, C(K, z)) is split into `world`
+contiguous pieces; rank g searches its piece of each level from z = K down and
+stops at its first level with a hit.  The global answer is the max over ranks
+of the key (z, -rank) -- one 8-byte all-reduce(MAX) over NCCL (the only
+collective; two tiny ones when K > 56 and the rank no longer fits the key).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from math import comb
+
+import numpy as np
+
+from . import _lib
+from .soa import requests_struct
+
+RANK_BITS = 57
+
+
+@dataclass
+class BruteResult:
+    z: int
+    lexrank: int
+    nodes_visited: int
+    mask: int
+
+
+def shard(total: int, world: int, rank: int):
+    """Contiguous piece `rank` of [0, total) split `world` ways."""
+    return total * rank // world, total * (rank + 1) // world
+
+
+def pack(z: int, r: int) -> int:
+    return (z << RANK_BITS) | ((1 << RANK_BITS) - 1 - r) if z else 0
+
+
+def unpack(key: int):
+    if key == 0:
+        return 0, -1
+    z = key >> RANK_BITS
+    return z, (1 << RANK_BITS) - 1 - (key & ((1 << RANK_BITS) - 1))
+
+
+def unrank(n: int, z: int, r: int) -> int:
+    """Bitmask of the r-th size-z combination of range(n) in lexicographic order."""
+    m, v = 0, 0
+    for j in range(z):
+        while True:
+            c = comb(n - v - 1, z - j - 1)
+            if r < c:
+                m |= 1 << v
+                v += 1
+                break
+            r -= c
+            v += 1
+    return m
+
+
+def nodes_for(n: int, z: int, r: int) -> int:
+    if z == 0:
+        return 2 ** n - 1 if n else 0
+    return sum(comb(n, q) for q in range(z + 1, n + 1)) + r + 1
+
+
+def device_level_range(ctx_rec: np.ndarray, cols: dict, device=None):
+    """Level evaluator on this process's GPU: (z, lo, hi) -> first feasible rank or -1."""
+    h = _lib.handle(device)
+    n = int(cols["prompt_tokens"].shape[0])
+    rs = requests_struct(cols)
+    ref = ctypes.cast(ctypes.pointer(rs), ctypes.c_void_p)
+
+    def level(z: int, lo: int, hi: int) -> int:
+        out = ctypes.c_int64(-1)
+        code = h.lib.eb_exhaustive_level_range(h.ptr, ctx_rec.ctypes.data, n, ref, z, lo, hi, ctypes.byref(out))
+        if code in (_lib.ERR_UPLINK_EFF_ZERO, _lib.ERR_DOWNLINK_EFF_ZERO):
+            raise ValueError("uplink spectral efficiency is zero" if code == _lib.ERR_UPLINK_EFF_ZERO
+                             else "downlink spectral efficiency is zero")
+        _lib.check(code, "eb_exhaustive_level_range")
+        return int(out.value)
+
+    return level
+
+
+def local_search(n: int, world: int, rank: int, level) -> tuple:
+    """This rank's best (z, r) over its shard of every level, searching z = n..1."""
+    for z in range(n, 0, -1):
+        lo, hi = shard(comb(n, z), world, rank)
+        if hi > lo:
+            r = level(z, lo, hi)
+            if r >= 0:
+                return z, r
+    return 0, -1
+
+
+def combine(keys) -> tuple:
+    """max over ranks of (z, -r)."""
+    best = (0, -1)
+    for z, r in keys:
+        if z > best[0] or (z == best[0] and z and r < best[1]):
+            best = (z, r)
+    return best
+
+
+def finish(n: int, z: int, r: int) -> BruteResult:
+    return BruteResult(z, r, nodes_for(n, z, r), unrank(n, z, r) if z else 0)
+
+
+def solve_sharded(ctx_rec, cols: dict, world: int, level=None, device=None) -> BruteResult:
+    """All `world` shards evaluated by this process in turn (single-GPU check of the sharding)."""
+    n = int(cols["prompt_tokens"].shape[0])
+    level = level or device_level_range(ctx_rec, cols, device)
+    return finish(n, *combine(local_search(n, world, g, level) for g in range(world)))
+
+
+def solve_distributed(ctx_rec, cols: dict, level=None, device=None, group=None) -> BruteResult:
+    """One shard per torch.distributed rank; a single all-reduce(MAX) of the packed key."""
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    n = int(cols["prompt_tokens"].shape[0])
+    level = level or device_level_range(ctx_rec, cols, device)
+    z, r = local_search(n, world, rank, level)
+    on_gpu = dist.get_backend(group) == "nccl"
+    tdev = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
+    if n <= 56:
+        key = torch.tensor([pack(z, r)], dtype=torch.int64, device=tdev)
+        dist.all_reduce(key, op=dist.ReduceOp.MAX, group=group)
+        zg, rg = unpack(int(key.item()))
+    else:
+        t = torch.tensor([z], dtype=torch.int64, device=tdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        zg = int(t.item())
+        rr = torch.tensor([r if (z == zg and zg) else 2 ** 62], dtype=torch.int64, device=tdev)
+        dist.all_reduce(rr, op=dist.ReduceOp.MIN, group=group)
+        rg = int(rr.item()) if zg else -1
+    return finish(n, zg, rg)

@@ -277,6 +277,8 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       if (O.counts) O.counts[inst * EB_MAX_CLASSES + lane] = 0;
       if (O.class_lengths) O.class_lengths[inst * EB_MAX_CLASSES + lane] = 0;
     }
+    if (O.solution)
+      for (int j = lane; j < n; j += 32) O.solution[r0 + j] = -1;
   };
 
   int ci = A.ctx_index ? A.ctx_index[inst] : 0;
@@ -680,6 +682,10 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       }
     }
   }
+  // rows past the batch are unused: mark them
+  if (O.solution)
+    for (int j = lane; j < n; j += 32)
+      if (!found || status != EB_OK || j >= zf) O.solution[r0 + j] = -1;
   if (lane == 0) {
     O.status[inst] = status;
     if (O.error_index) O.error_index[inst] = -1;
@@ -792,9 +798,11 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   A.ctx_index = d_ctx_index; A.req_base = req_base; A.req = d_req; A.K = K; A.G = G;
   A.warp_bytes = al8(dftsp_warp_bytes(K, G, exact));
   A.out = d_out; A.traj_base = traj_base; A.counter = d_counter;
-  const int warps = 4;
+  const size_t smem_cap = 227 * 1024;
+  int warps = (int)(smem_cap / A.warp_bytes);
+  if (warps > 4) warps = 4;
+  if (warps < 1) { set_error("instance size K=%d needs %zu B shared memory per warp", K, A.warp_bytes); return EB_ERR_K_TOO_LARGE; }
   size_t smem = A.warp_bytes * warps;
-  if (smem > 227 * 1024) { set_error("instance size K=%d needs %zu B shared memory per block", K, smem); return EB_ERR_K_TOO_LARGE; }
   void (*kern)(DftspArgs);
   const bool P = prm.pruning != 0, I = prm.inclusive_bound != 0;
   if (P) {
