@@ -36,6 +36,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))   # CPU baseline / reference arm only
 
 FP64_LANES_PER_SM = 64          # B200 FP64 pipe: 64 lanes/SM/clk
 LEAF_OPS, DESCEND_OPS = 26, 5   # algorithmic FP64-class ops per leaf check / descend

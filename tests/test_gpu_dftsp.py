@@ -89,14 +89,32 @@ def test_gpu_trajectory_matches_reference():
 
 
 def test_gpu_k64_and_sixteen_classes():
-    """Device limits: 64 candidates, 16 output classes (no ladder)."""
+    """Device limits: 64 candidates over 16 output classes (no ladder).  A
+    roomy node makes the top levels feasible so the search (and the oracle)
+    terminates; the partition/table machinery still runs at full width."""
     batch, _ = random_batch(99, 6, k_min=64, k_max=64, max_classes=5)
-    # spread outputs over 16 distinct lengths
     rng = np.random.default_rng(1)
     batch.columns["output_tokens"][:] = rng.choice(np.arange(1, 17) * 8, size=batch.n_req)
+    batch.columns["deadline_s"][:] = 1e6
+    batch.columns["channel_gain"][:] = 1.0
+    for c in batch.contexts:
+        c["memory_bytes"] *= 1e6
+        c["flops_per_s"] *= 1e6
+        c["uplink_band_hz"] = c["downlink_band_hz"] = 1e9
+        c["has_slot_cap"] = 0
     dev = search.solve_batch(batch, ladder=None)
     orc = oracle.dftsp_batch(batch, ladder=None, threads=6)
     _assert_same(dev, orc, batch, "K=64, 16 classes")
+    assert (dev.z_found > 40).all()
+
+
+def test_gpu_k64_three_classes_deep_search():
+    """K = 64 with three classes: thousands of dfs calls per instance."""
+    batch, ladders = random_batch(98, 8, k_min=60, k_max=64, max_classes=3)
+    for lad, (idx, sb) in group_by_ladder(batch, ladders).items():
+        dev = search.solve_batch(sb, ladder=lad)
+        orc = oracle.dftsp_batch(sb, ladder=lad, threads=8)
+        _assert_same(dev, orc, sb, f"K=64 ladder {lad}")
 
 
 def test_gpu_edge_statuses():
