@@ -111,6 +111,10 @@ typedef struct eb_search_params {
   int32_t collect_trajectory; /* default 0 */
   int32_t ladder_len;         /* 0 = ladder None */
   int32_t ladder[EB_MAX_CLASSES];
+  /* Device algorithm (results are identical): 0 = auto (leaf-parallel when
+   * its tables fit), 1 = one dfs call per lane (literal node walk),
+   * 2 = leaf-parallel enumeration with combinatorial node counts. */
+  int32_t algorithm;
 } eb_search_params;
 
 /* Indices into eb_dftsp_result.metrics[i*EB_N_METRICS + m]. */

@@ -344,7 +344,7 @@ int32_t eb_dftsp_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, cons
       d_out.traj = S->alloc<int64_t>((size_t)nt * 4);
       d_out.traj_len = S->out(out->traj_len, ni);
     }
-    int* d_counter = S->alloc<int>(1);
+    int* d_counter = S->alloc<int>(2);
     if (S->err) { rc = S->err; break; }
     rc = launch_dftsp(h, st, d_ctx[c % 3], n_ctx, *prm, ni, d_off, d_ci, R0, d_req, K, d_out, T0, d_counter);
     if (rc) break;

@@ -28,6 +28,7 @@ namespace eb {
 namespace {
 
 constexpr int RING = 64;  // in-flight window of dfs calls per warp
+constexpr int EB_STATUS_FALLBACK = 99;  // internal: v2 tables overflowed, v1 pass pending
 
 struct __align__(8) LevelInfo {
   uint16_t off;       // table offset (entries) of x = 0 for this class
@@ -49,11 +50,12 @@ struct Lay {
   size_t sizes, ncls, lvl;                                  // per pool width d
   size_t t_up, t_dn, t_tau;                                 // prefix tables
   size_t ring_v, ring_p, ring_done, sol;
+  size_t pq, pre, pf;                                       // v2: unranking / call prefix / F tables
   size_t total;
   int T;
 };
 
-__host__ __device__ inline Lay make_lay(int K, int G, bool exact) {
+__host__ __device__ inline Lay make_lay(int K, int G, bool exact, bool v2) {
   Lay L;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = al8(o + bytes); return r; };
@@ -69,6 +71,14 @@ __host__ __device__ inline Lay make_lay(int K, int G, bool exact) {
   L.t_tau = exact ? take(8 * (size_t)L.T) : 0;
   L.ring_v = take(8 * RING); L.ring_p = take(8 * RING); L.ring_done = take(RING);
   L.sol = take(K);
+  if (v2) {
+    const int lvls = G > 1 ? G - 1 : 1;
+    L.pq = take(4 * (size_t)K * lvls * (K + 2));
+    L.pre = take(4 * (size_t)(K + 2));
+    L.pf = take(16 * (size_t)G * (K + 1));
+  } else {
+    L.pq = L.pre = L.pf = 0;
+  }
   L.total = o;
   return L;
 }
@@ -86,7 +96,8 @@ struct DftspArgs {
   size_t warp_bytes;
   eb_dftsp_result out;        // per-instance arrays launch-local; solution at row - req_base
   int64_t traj_base;          // absolute row of out.traj element 0
-  int* counter;
+  int* counter;               // [0] instance queue, [1] fallback count
+  int fallback_pass;
 };
 
 __device__ __forceinline__ int getV(uint64_t v0, uint64_t v1, int k) {
@@ -221,11 +232,338 @@ __device__ __forceinline__ int dfs_step(Lane& s, const Tables& T) {
   return 0;
 }
 
+
+// ===========================================================================
+// v2 search: leaf-parallel enumeration with combinatorial node counting.
+//
+// Facts used (all from the dfs loop, dftsp.py:183-234):
+//  * the leaves of dfs(z) on a partition are exactly the count vectors c
+//    (0 <= c_k <= s_k, sum c = z), met in lexicographically descending order;
+//    the leaf check (dftsp.py:193-203) is a pure function of c (the
+//    accumulator chain is a left fold over the classes; trailing zero counts
+//    add +0.0, which is exact);
+//  * every other step is data independent, so the node counts of a fully
+//    searched (failed) subtree depend only on the class sizes, the remaining
+//    target and the flags: F(k, r) below, a per-level recurrence over prefix
+//    sums that restates the prune / visit / dead-end / descend rules;
+//  * therefore the reference's first successful (z, d, leaf) in sequence
+//    order can be found by evaluating leaves in parallel (32 per warp step,
+//    in order, ballot + first set lane), and nodes_visited / nodes_pruned
+//    are sum F over the failed calls plus the partial count of the winning
+//    call up to its leaf.
+//  * the first leaf of a call is the greedy low-output fill, which minimises
+//    the memory sum (exact integers) and the latency sum (weights ascend with
+//    the output length); a call whose greedy leaf fails memory or latency by
+//    a margin far beyond floating-point error cannot contain a passing leaf
+//    and is skipped without enumeration (its node counts are still added).
+// ===========================================================================
+__device__ __forceinline__ bool fails_with_margin(double a_lo, double b) {
+  // true only if leq(a, b) is false for every a >= a_lo (leq is monotone in a)
+  double m = 1.0;
+  double aa = fabs_(a_lo), ab = fabs_(b);
+  if (aa > m) m = aa;
+  if (ab > m) m = ab;
+  return sub(a_lo, b) > mul(1.00001e-9, m);
+}
+
+// Blocked warp-wide inclusive prefix over r = 0..n of two u64 sequences.
+template <typename ValFn, typename StoreFn>
+__device__ __forceinline__ void warp_prefix2(int n, ValFn val, StoreFn store) {
+  const int lane = threadIdx.x & 31;
+  const int q = (n + 32) >> 5;                 // ceil((n + 1) / 32) <= 3
+  uint64_t va[3], vb[3], la = 0, lb = 0;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    int r = lane * q + j;
+    va[j] = vb[j] = 0;
+    if (j < q && r <= n) val(r, va[j], vb[j]);
+    la += va[j];
+    lb += vb[j];
+  }
+  uint64_t ia = la, ib = lb;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t ta = __shfl_up_sync(EB_FULL, ia, o), tb = __shfl_up_sync(EB_FULL, ib, o);
+    if (lane >= o) { ia += ta; ib += tb; }
+  }
+  uint64_t ra = ia - la, rb = ib - lb;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    int r = lane * q + j;
+    if (j < q && r <= n) { ra += va[j]; rb += vb[j]; store(r, ra, rb); }
+  }
+}
+
+// Full-traversal node counts of one dfs level (dftsp.py:183-234) entered at
+// level k with remaining target r >= 1: (visited, pruned).  PF* = prefix
+// sums over r of F(k+1, .) (index r, F(., 0) = 0).
+template <bool PRUNE, bool INCL>
+__device__ __forceinline__ void level_counts(const LevelInfo& li, bool last, int r, const uint64_t* PFV,
+                                             const uint64_t* PFP, uint64_t& fv, uint64_t& fp) {
+  const int s = li.size, cap = li.tail_next + (INCL ? li.size : 0);
+  const int x0 = min(r, s);
+  const int xs = PRUNE ? max(0, r - cap) : 0;          // lowest unpruned count
+  if (PRUNE && x0 < xs) { fv = 0; fp = (uint64_t)x0 + 1; return; }
+  if (last) {
+    if (x0 == r) {                                      // leaf, then x = r - 1
+      if (PRUNE && r - 1 < xs) { fv = 1; fp = (uint64_t)r; }
+      else { fv = 1 + (uint64_t)r; fp = 0; }            // dead end: 1 + bulk (r - 1)
+    } else {
+      fv = 1 + (uint64_t)x0; fp = 0;                    // dead end at x0
+    }
+    return;
+  }
+  fv = (uint64_t)(x0 - xs + 1);                         // nodes x = x0 .. xs visited
+  fp = (PRUNE && xs > 0) ? (uint64_t)xs : 0;            // prune event at x = xs - 1
+  const int xb = (x0 == r) ? x0 - 1 : x0;               // descending nodes x = xb .. xs
+  if (xb >= xs) {
+    fv += PFV[r - xs] - PFV[r - xb - 1];
+    fp += PFP[r - xs] - PFP[r - xb - 1];
+  }
+}
+
 template <bool PRUNE, bool INCL, bool EXACT>
+__device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, const LevelInfo* lvl,
+                          const uint8_t* ncls_d, const double* t_up, const double* t_dn, const double* t_tau,
+                          const int32_t* c_len, const double* c_w, const double* o_tau, double k2, double k3,
+                          double slot_base, bool has_cap, int padded, int64_t* traj, bool& found, int& zf,
+                          int& dwin, int& kwin, uint64_t& W0, uint64_t& W1, int& best, uint64_t& tot_v,
+                          uint64_t& tot_p) {
+  const int lane = threadIdx.x & 31;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  uint32_t* pq = (uint32_t*)(smem + L.pq);
+  uint32_t* pre = (uint32_t*)(smem + L.pre);
+  uint64_t* pfv = (uint64_t*)(smem + L.pf);
+  uint64_t* pfp = pfv + (size_t)Gi * (n + 1);
+  const int LV = Gi > 1 ? Gi - 1 : 1;
+  const int W = n + 2;
+
+  // ---- U: unranking tables.  For partition d and level k >= 1,
+  //      PQ_k[x + 1] = #{(c_k..c_{m-1}) : bounds, sum <= x}  (prefix of Q_k).
+  bool ovf = false;
+  for (int d = 1; d <= n; ++d) {
+    const int m = ncls_d[d - 1];
+    if (m < 2) continue;
+    const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
+    uint32_t* base = pq + (size_t)(d - 1) * LV * W;
+    {
+      uint32_t* P = base + (size_t)(m - 2) * W;         // level m-1: Q(r) = [r <= s]
+      const int sl = row[m - 1].size;
+      for (int x = lane; x <= n + 1; x += 32) P[x] = (x == 0) ? 0u : (uint32_t)(min(x - 1, sl) + 1);
+    }
+    __syncwarp();
+    for (int k = m - 2; k >= 1; --k) {
+      const uint32_t* Pn = base + (size_t)k * W;        // level k+1
+      uint32_t* Pk = base + (size_t)(k - 1) * W;        // level k
+      const int sk = row[k].size;
+      bool o2 = false;
+      warp_prefix2(n,
+          [&](int r, uint64_t& a, uint64_t& b) {
+            int lo = r - sk - 1;
+            a = (uint64_t)Pn[r + 1] - (lo >= 0 ? (uint64_t)Pn[lo + 1] : 0);
+            b = 0;
+          },
+          [&](int r, uint64_t a, uint64_t) {
+            if (a > 0x7fffffffULL) o2 = true;
+            Pk[r + 1] = (uint32_t)a;
+          });
+      if (lane == 0) Pk[0] = 0;
+      ovf |= __any_sync(EB_FULL, o2);
+      __syncwarp();
+    }
+  }
+  if (ovf) return false;
+
+  // ---- S: leaves in sequence order (z from n down, d from z up, lex-desc)
+  found = false;
+  for (int z = n; z >= 1 && !found; --z) {
+    const double k3z = mul(k3, i2d(z));                            // coeff.k3 * z
+    const double slot_cap = has_cap ? sub(slot_base, k3z) : INF;  // slot_budget(z)
+    const double mem_cap = sub(k2, i2d((int64_t)padded * z));      // mem_budget(z)
+    const int nd = n - z + 1;
+    uint32_t cnt[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int d = z + lane + 32 * h;
+      if (d > n) continue;
+      const int m = ncls_d[d - 1];
+      const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
+      uint32_t N;
+      if (m == 1) {
+        N = (z <= row[0].size) ? 1u : 0u;
+      } else {
+        const uint32_t* P1 = pq + (size_t)(d - 1) * LV * W;        // level 1
+        const int hi0 = min(z, (int)row[0].size), lo0 = max(0, z - (int)row[0].tail_next);
+        N = (hi0 >= lo0) ? P1[z - lo0 + 1] - P1[z - hi0] : 0u;
+      }
+      // sound skip: greedy (first) leaf fails memory or latency by a margin
+      int rem = z;
+      int64_t mem = 0;
+      double lat = 0.0;
+      for (int k = 0; k < m; ++k) {
+        const LevelInfo li = row[k];
+        const int c = min(rem, (int)li.size);
+        mem += (int64_t)c * c_len[li.g];
+        lat = add(lat, mul(i2d(c), c_w[li.g]));
+        rem -= c;
+      }
+      const double lat_cap = EXACT ? slot_cap : pymin(sub(o_tau[d - 1], k3z), slot_cap);
+      const bool skip = fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap);
+      cnt[h] = skip ? 0u : N;
+    }
+    // exclusive prefix of cnt over d = z..n (lane order, then +32)
+    uint32_t inc0 = cnt[0], inc1 = cnt[1];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t t0 = __shfl_up_sync(EB_FULL, inc0, o), t1 = __shfl_up_sync(EB_FULL, inc1, o);
+      if (lane >= o) { inc0 += t0; inc1 += t1; }
+    }
+    const uint32_t tot0 = __shfl_sync(EB_FULL, inc0, 31);
+    inc1 += tot0;
+    const uint32_t T = __shfl_sync(EB_FULL, inc1, 31);
+    if (lane < nd) pre[lane] = inc0 - cnt[0];
+    if (lane + 32 < nd) pre[lane + 32] = inc1 - cnt[1];
+    __syncwarp();
+    for (uint32_t b0 = 0; b0 < T; b0 += 32) {
+      const uint32_t g = b0 + lane;
+      bool pass = false;
+      int d = 0, klast = 0;
+      uint64_t V0 = 0, V1 = 0;
+      if (g < T) {
+        int a = 0, bnd = nd - 1;                                   // largest idx with pre[idx] <= g
+        while (a < bnd) {
+          int mid = (a + bnd + 1) >> 1;
+          if (pre[mid] <= g) a = mid; else bnd = mid - 1;
+        }
+        d = z + a;
+        uint32_t i = g - pre[a];
+        const int m = ncls_d[d - 1];
+        const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
+        const uint32_t* base = pq + (size_t)(d - 1) * LV * W;
+        int r = z;
+        double u = 0.0, dl = 0.0, lat = 0.0, tau = INF;
+        int64_t mem = 0;
+        for (int k = 0; k < m; ++k) {
+          const LevelInfo li = row[k];
+          int c;
+          if (k == m - 1) {
+            c = r;
+          } else {                                                 // unrank level k
+            const uint32_t* P = base + (size_t)k * W;              // level k+1 prefix
+            const int hi = min(r, (int)li.size), lo = max(0, r - (int)li.tail_next);
+            const uint32_t pb = P[r - hi];
+            int xa = r - hi, xz = r - lo;
+            while (xa < xz) {
+              int mid = (xa + xz) >> 1;
+              if (P[mid + 1] - pb > i) xz = mid; else xa = mid + 1;
+            }
+            i -= P[xa] - pb;
+            c = r - xa;
+          }
+          if (c) { setV(V0, V1, k, c); klast = k; }
+          u = add(u, t_up[li.off + c]);                            // up_acc + up[k][x]
+          dl = add(dl, t_dn[li.off + c]);
+          mem += (int64_t)c * c_len[li.g];
+          lat = add(lat, mul(i2d(c), c_w[li.g]));
+          if (EXACT && c) tau = pymin(tau, t_tau[li.off + c]);
+          r -= c;
+        }
+        const double cap = EXACT ? pymin(sub(tau, k3z), slot_cap) : pymin(sub(o_tau[d - 1], k3z), slot_cap);
+        pass = leq(u, 1.0) && leq(dl, 1.0) && leq(i2d(mem), mem_cap) && leq(lat, cap);
+      }
+      const unsigned bal = __ballot_sync(EB_FULL, pass);
+      if (bal) {
+        const int src = __ffs(bal) - 1;
+        found = true;
+        zf = z;
+        dwin = __shfl_sync(EB_FULL, d, src);
+        kwin = __shfl_sync(EB_FULL, klast, src);
+        W0 = __shfl_sync(EB_FULL, V0, src);
+        W1 = __shfl_sync(EB_FULL, V1, src);
+        break;
+      }
+    }
+    __syncwarp();
+  }
+  best = found ? (n - zf) * (n - zf + 1) / 2 + (dwin - zf) : INT_MAX;
+
+  // ---- C: node counts.  Calls (z, d) counted: z > zf (all d >= z), and
+  //      z == zf with d < dwin; plus the winner's partial count.
+  uint64_t my_v = 0, my_p = 0;
+  for (int d = found ? zf : 1; d <= n; ++d) {
+    const int m = ncls_d[d - 1];
+    const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
+    for (int k = m - 1; k >= 1; --k) {
+      const uint64_t* NV = pfv + (size_t)(k + 1) * (n + 1);
+      const uint64_t* NP = pfp + (size_t)(k + 1) * (n + 1);
+      uint64_t* KV = pfv + (size_t)k * (n + 1);
+      uint64_t* KP = pfp + (size_t)k * (n + 1);
+      const LevelInfo li = row[k];
+      const bool last = (k == m - 1);
+      warp_prefix2(n,
+          [&](int r, uint64_t& a, uint64_t& b) {
+            if (r == 0) { a = b = 0; return; }
+            level_counts<PRUNE, INCL>(li, last, r, NV, NP, a, b);
+          },
+          [&](int r, uint64_t a, uint64_t b) { KV[r] = a; KP[r] = b; });
+      __syncwarp();
+    }
+    const LevelInfo l0 = row[0];
+    for (int r = 1 + lane; r <= d; r += 32) {
+      const bool win = found && r == zf && d == dwin;
+      const bool counted = !found || r > zf || (r == zf && d < dwin);
+      if (!win && !counted) continue;
+      uint64_t fv, fp;
+      if (!win) {
+        level_counts<PRUNE, INCL>(l0, m == 1, r, pfv + (size_t)(n + 1), pfp + (size_t)(n + 1), fv, fp);
+        fv += 1;                                                   // the root
+      } else {
+        // nodes before the winning leaf: root, then per level j < kwin the
+        // earlier siblings x in (c_j, x0_j] with their full subtrees, the path
+        // node c_j; finally the leaf itself (first node of level kwin).
+        fv = 1;
+        fp = 0;
+        int rr = r;
+        for (int j = 0; j < kwin; ++j) {
+          const LevelInfo lj = row[j];
+          const int c = getV(W0, W1, j);
+          const int x0 = min(rr, (int)lj.size);
+          const int xb = (x0 == rr) ? x0 - 1 : x0;
+          fv += (uint64_t)(x0 - c) + 1;
+          if (xb >= c + 1) {
+            const uint64_t* SV = pfv + (size_t)(j + 1) * (n + 1);
+            const uint64_t* SP = pfp + (size_t)(j + 1) * (n + 1);
+            fv += SV[rr - c - 1] - SV[rr - xb - 1];
+            fp += SP[rr - c - 1] - SP[rr - xb - 1];
+          }
+          rr -= c;
+        }
+        fv += 1;
+      }
+      my_v += fv;
+      my_p += fp;
+      if (traj) {
+        int64_t* tr = traj + 4 * (int64_t)((n - r) * (n - r + 1) / 2 + (d - r));
+        tr[0] = r; tr[1] = d; tr[2] = (int64_t)fv; tr[3] = (int64_t)fp;
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    my_v += __shfl_xor_sync(EB_FULL, my_v, o);
+    my_p += __shfl_xor_sync(EB_FULL, my_p, o);
+  }
+  tot_v = my_v;
+  tot_p = my_p;
+  return true;
+}
+
+template <bool PRUNE, bool INCL, bool EXACT, int ALGO>
 __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* smem) {
   const int lane = threadIdx.x & 31;
   const int K = A.K, G = A.G;
-  const Lay L = make_lay(K, G, EXACT);
+  const Lay L = make_lay(K, G, EXACT, ALGO == 2);
   double* a_tau = (double*)(smem + L.a_tau);
   double* a_key = (double*)(smem + L.a_key);
   int64_t* a_id = (int64_t*)(smem + L.a_id);
@@ -530,12 +868,28 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   if (lane < RING / 32 * 32) { ring_done[lane] = 0; ring_done[lane + 32] = 0; }
   __syncwarp();
 
-  // ---------------- search: lanes = dfs calls in sequence order ----------
+  // ---------------- search ------------------------------------------------
   const int total_calls = n * (n + 1) / 2;
   const bool collect = A.prm.collect_trajectory && O.traj && O.traj_offsets;
   int64_t* traj = collect ? O.traj + 4 * (O.traj_offsets[inst] - A.traj_base) : nullptr;
-  int next_call = 0, best = INT_MAX, fold = 0;
+  int best = INT_MAX;                // sequence index of the winning dfs call
   uint64_t tot_v = 0, tot_p = 0;
+  bool found = false;
+  int zf = 0, dwin = 0, kwin = 0;
+  uint64_t W0 = 0, W1 = 0;
+  if constexpr (ALGO == 2) {
+    if (!search_v2<PRUNE, INCL, EXACT>(n, Gi, smem, L, lvl, ncls_d, t_up, t_dn, t_tau, c_len, c_w, o_tau, k2, k3,
+                                       slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
+                                       tot_v, tot_p)) {
+      // leaf counts overflow the u32 unranking tables: hand the instance to
+      // the literal walk (second pass of launch_dftsp)
+      put_status(EB_STATUS_FALLBACK, -1);
+      if (lane == 0) atomicAdd(A.counter + 1, 1);
+      return;
+    }
+  } else {
+  int next_call = 0, fold = 0;
+  tot_v = 0; tot_p = 0;
 
   Lane S;
   S.z = S.k = S.x = S.sel = S.ncl = 0;
@@ -603,11 +957,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     }
     if (best != INT_MAX ? fold > best : fold >= total_calls) break;
   }
-
-  // ---------------- finish ------------------------------------------------
-  const bool found = best != INT_MAX;
-  int zf = 0, dwin = 0, kwin = 0;
-  uint64_t W0 = 0, W1 = 0;
+  found = best != INT_MAX;
   if (found) {
     unsigned who = __ballot_sync(EB_FULL, succ_c == best);
     int src = __ffs(who) - 1;
@@ -617,6 +967,9 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     W0 = __shfl_sync(EB_FULL, succ_V0, src);
     W1 = __shfl_sync(EB_FULL, succ_V1, src);
   }
+  }  // v1
+
+  // ---------------- finish ------------------------------------------------
   int status = EB_OK;
   double met[EB_N_METRICS];
 #pragma unroll
@@ -709,17 +1062,21 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   }
 }
 
-template <bool PRUNE, bool INCL, bool EXACT>
+template <bool PRUNE, bool INCL, bool EXACT, int ALGO>
 __global__ void __launch_bounds__(128) dftsp_kernel(DftspArgs A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   const int warp = threadIdx.x >> 5;
   unsigned char* smem = smem_all + warp * A.warp_bytes;
+  // second (fallback) pass: only instances v2 flagged, and nothing at all
+  // when none were flagged
+  if (A.fallback_pass && *(volatile int*)(A.counter + 1) == 0) return;
   for (;;) {
     int64_t inst = 0;
     if ((threadIdx.x & 31) == 0) inst = atomicAdd(A.counter, 1);
     inst = __shfl_sync(EB_FULL, inst, 0);
     if (inst >= A.n_inst) break;
-    solve_instance<PRUNE, INCL, EXACT>(A, inst, smem);
+    if (A.fallback_pass && A.out.status[inst] != EB_STATUS_FALLBACK) continue;
+    solve_instance<PRUNE, INCL, EXACT, ALGO>(A, inst, smem);
     __syncwarp();
   }
 }
@@ -783,7 +1140,22 @@ __global__ void dfs_single_kernel(int z, int ncls, const int32_t* sizes, const i
 // ---------------------------------------------------------------------------
 // Host-side launcher (device pointers, caller's stream).
 // ---------------------------------------------------------------------------
-size_t dftsp_warp_bytes(int K, int G, bool exact) { return make_lay(K, G, exact).total; }
+size_t dftsp_warp_bytes(int K, int G, bool exact) { return make_lay(K, G, exact, true).total; }
+
+static int launch_one(eb_handle* h, cudaStream_t st, void (*kern)(DftspArgs), const DftspArgs& A, int warps,
+                      size_t smem, int64_t n_inst) {
+  EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));
+  if (per_sm < 1) per_sm = 1;
+  int64_t want = (n_inst + warps - 1) / warps;
+  int64_t grid = (int64_t)per_sm * h->num_sms;
+  if (grid > want) grid = want;
+  kern<<<(unsigned)grid, 32 * warps, smem, st>>>(A);
+  EB_CUDA(cudaGetLastError());
+  h->launches += 1;
+  return EB_OK;
+}
 
 int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_ctx,
                  const eb_search_params& prm, int64_t n_inst, const int64_t* d_off,
@@ -796,34 +1168,43 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   DftspArgs A;
   A.ctxs = d_ctxs; A.n_ctx = n_ctx; A.prm = prm; A.n_inst = n_inst; A.offsets = d_off;
   A.ctx_index = d_ctx_index; A.req_base = req_base; A.req = d_req; A.K = K; A.G = G;
-  A.warp_bytes = al8(dftsp_warp_bytes(K, G, exact));
-  A.out = d_out; A.traj_base = traj_base; A.counter = d_counter;
+  // algorithm: 2 = leaf-parallel (default) unless its tables do not fit two
+  // warps per block, 1 = literal lanes-per-call (also v2's in-kernel fallback)
+  int algo = prm.algorithm;
   const size_t smem_cap = 227 * 1024;
+  if (algo != 1 && al8(make_lay(K, G, exact, true).total) * 2 > smem_cap) algo = 1;
+  if (algo != 1) algo = 2;
+  A.warp_bytes = al8(make_lay(K, G, exact, algo == 2).total);
   int warps = (int)(smem_cap / A.warp_bytes);
   if (warps > 4) warps = 4;
   if (warps < 1) { set_error("instance size K=%d needs %zu B shared memory per warp", K, A.warp_bytes); return EB_ERR_K_TOO_LARGE; }
   size_t smem = A.warp_bytes * warps;
   void (*kern)(DftspArgs);
   const bool P = prm.pruning != 0, I = prm.inclusive_bound != 0;
-  if (P) {
-    if (I) kern = exact ? dftsp_kernel<true, true, true> : dftsp_kernel<true, true, false>;
-    else kern = exact ? dftsp_kernel<true, false, true> : dftsp_kernel<true, false, false>;
-  } else {
-    if (I) kern = exact ? dftsp_kernel<false, true, true> : dftsp_kernel<false, true, false>;
-    else kern = exact ? dftsp_kernel<false, false, true> : dftsp_kernel<false, false, false>;
+#define EB_PICK(AL)                                                                              \
+  if (P) {                                                                                       \
+    if (I) kern = exact ? dftsp_kernel<true, true, true, AL> : dftsp_kernel<true, true, false, AL>; \
+    else kern = exact ? dftsp_kernel<true, false, true, AL> : dftsp_kernel<true, false, false, AL>; \
+  } else {                                                                                       \
+    if (I) kern = exact ? dftsp_kernel<false, true, true, AL> : dftsp_kernel<false, true, false, AL>; \
+    else kern = exact ? dftsp_kernel<false, false, true, AL> : dftsp_kernel<false, false, false, AL>; \
   }
-  EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));
-  if (per_sm < 1) per_sm = 1;
-  int64_t want = (n_inst + warps - 1) / warps;
-  int64_t grid = (int64_t)per_sm * h->num_sms;
-  if (grid > want) grid = want;
+  if (algo == 2) { EB_PICK(2) } else { EB_PICK(1) }
+  A.fallback_pass = 0;
+  EB_CUDA(cudaMemsetAsync(d_counter, 0, 2 * sizeof(int), st));
+  int rc = launch_one(h, st, kern, A, warps, smem, n_inst);
+  if (rc || algo != 2) return rc;
+  // literal-walk pass for any instance whose leaf counts overflowed u32
+  DftspArgs B = A;
+  B.fallback_pass = 1;
+  B.warp_bytes = al8(make_lay(K, G, exact, false).total);
+  int wb = (int)(smem_cap / B.warp_bytes);
+  if (wb > 4) wb = 4;
+  EB_PICK(1)
   EB_CUDA(cudaMemsetAsync(d_counter, 0, sizeof(int), st));
-  kern<<<(unsigned)grid, 32 * warps, smem, st>>>(A);
-  EB_CUDA(cudaGetLastError());
-  h->launches += 1;
-  return EB_OK;
+  int rc2 = launch_one(h, st, kern, B, wb, B.warp_bytes * wb, n_inst);
+#undef EB_PICK
+  return rc2;
 }
 
 int launch_dfs_single(eb_handle* h, cudaStream_t st, int z, int ncls, const int32_t* sizes,

@@ -194,8 +194,11 @@ class BatchResult:
 
 
 def solve_batch(batch: InstanceBatch, *, pruning=True, inclusive_bound=False, exact_tau=False,
-                collect_trajectory=False, ladder=None, device=None, handle=None) -> BatchResult:
-    """K3 over a host InstanceBatch: every instance is one dftsp() call."""
+                collect_trajectory=False, ladder=None, device=None, handle=None, algorithm=0) -> BatchResult:
+    """K3 over a host InstanceBatch: every instance is one dftsp() call.
+
+    ``algorithm``: 0 auto, 1 literal node walk (one dfs call per lane), 2
+    leaf-parallel with combinatorial node counts -- identical results."""
     n, nr = batch.n_inst, batch.n_req
     sizes = np.diff(batch.offsets)
     res = BatchResult(status=np.zeros(n, np.int32), error_index=np.full(n, -1, np.int32),
@@ -217,7 +220,7 @@ def solve_batch(batch: InstanceBatch, *, pruning=True, inclusive_bound=False, ex
         out.traj_offsets = res.traj_offsets.ctypes.data
         out.traj = res.traj.ctypes.data
         out.traj_len = res.traj_len.ctypes.data
-    prm = search_params(pruning, inclusive_bound, exact_tau, collect_trajectory, ladder)
+    prm = search_params(pruning, inclusive_bound, exact_tau, collect_trajectory, ladder, algorithm)
     h = handle or _lib.handle(device)
     b = batch.struct()
     _lib.check(h.lib.eb_dftsp_batch(h.ptr, batch.contexts.ctypes.data, len(batch.contexts), _ref(prm), _ref(b),

@@ -136,8 +136,10 @@ class InstanceBatch:
         return cls(offsets, cols, contexts, ci, max(sizes) if sizes else 1)
 
 
-def search_params(pruning=True, inclusive_bound=False, exact_tau=False, collect_trajectory=False, ladder=None):
+def search_params(pruning=True, inclusive_bound=False, exact_tau=False, collect_trajectory=False, ladder=None,
+                  algorithm=0):
     p = _lib.eb_search_params()
+    p.algorithm = int(algorithm)
     p.pruning = int(bool(pruning))
     p.inclusive_bound = int(bool(inclusive_bound))
     p.exact_tau = int(bool(exact_tau))

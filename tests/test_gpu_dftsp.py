@@ -16,16 +16,17 @@ pytestmark = pytest.mark.gpu
 RES_KEYS = ("status", "z_found", "nodes_visited", "nodes_pruned", "n_classes", "counts", "class_lengths")
 
 
-def _gpu_solve(batch, ladder=None, **flags):
-    return search.solve_batch(batch, ladder=ladder, **flags)
-
-
+@pytest.mark.parametrize("algo", [1, 2])
 @pytest.mark.parametrize("name", ALL_CORPORA)
-def test_gpu_matches_reference_goldens(name):
+def test_gpu_matches_reference_goldens(name, algo):
     if not os.path.exists(corpus_path(name)):
         pytest.skip("corpus missing")
     d = load_corpus(name)
     tags = [t for t in FLAGS if f"{t}_z" in d]
+
+    def _gpu_solve(batch, ladder=None, **flags):
+        return search.solve_batch(batch, ladder=ladder, algorithm=algo, **flags)
+
     for tag in tags:
         bad = compare_corpus(d, tag, _gpu_solve, use_ladder=(tag != "NL"))
         assert not bad, f"{name}/{tag}: {bad[:3]}"
@@ -45,29 +46,33 @@ def _assert_same(dev, orc, batch, what):
         assert np.array_equal(dev.metrics[i], orc["metrics"][i]), f"{what}: metrics {i}"
 
 
+@pytest.mark.parametrize("algo", [1, 2])
 @pytest.mark.parametrize("seed", [11, 12, 13])
 @pytest.mark.parametrize("tag", ["P", "NP", "PI", "PE"])
-def test_gpu_matches_oracle_fresh_corpora(seed, tag):
-    batch, ladders = random_batch(1000 * seed + hash(tag) % 97, 600)
+def test_gpu_matches_oracle_fresh_corpora(seed, tag, algo):
+    batch, ladders = random_batch(1000 * seed + sum(map(ord, tag)), 600)
     for lad, (idx, sb) in group_by_ladder(batch, ladders).items():
-        dev = search.solve_batch(sb, ladder=lad, **FLAGS[tag])
+        dev = search.solve_batch(sb, ladder=lad, algorithm=algo, **FLAGS[tag])
         orc = oracle.dftsp_batch(sb, ladder=lad, threads=8, **FLAGS[tag])
         _assert_same(dev, orc, sb, f"seed {seed} {tag} ladder {lad}")
 
 
 def test_gpu_matches_oracle_no_ladder_many_classes():
     batch, _ = random_batch(77, 400, k_max=20, max_classes=5)
-    dev = search.solve_batch(batch, ladder=None)
-    orc = oracle.dftsp_batch(batch, ladder=None, threads=8)
-    _assert_same(dev, orc, batch, "no ladder, <=5 classes")
+    for algo in (1, 2):
+        dev = search.solve_batch(batch, ladder=None, algorithm=algo)
+        orc = oracle.dftsp_batch(batch, ladder=None, threads=8)
+        _assert_same(dev, orc, batch, f"no ladder, <=5 classes, algo {algo}")
 
 
-def test_gpu_large_k_and_trajectory():
+@pytest.mark.parametrize("algo", [1, 2])
+@pytest.mark.parametrize("tag", ["P", "NP", "PI"])
+def test_gpu_large_k_and_trajectory(algo, tag):
     batch, ladders = random_batch(5, 120, k_min=30, k_max=48, max_classes=4)
     for lad, (idx, sb) in group_by_ladder(batch, ladders).items():
-        dev = search.solve_batch(sb, ladder=lad, collect_trajectory=True)
-        orc = oracle.dftsp_batch(sb, ladder=lad, collect_trajectory=True, threads=8)
-        _assert_same(dev, orc, sb, f"K 30-48 ladder {lad}")
+        dev = search.solve_batch(sb, ladder=lad, collect_trajectory=True, algorithm=algo, **FLAGS[tag])
+        orc = oracle.dftsp_batch(sb, ladder=lad, collect_trajectory=True, threads=8, **FLAGS[tag])
+        _assert_same(dev, orc, sb, f"K 30-48 ladder {lad} {tag} algo {algo}")
         assert np.array_equal(dev.traj_len, orc["traj_len"])
         for j in range(sb.n_inst):
             t0 = int(dev.traj_offsets[j])
@@ -75,13 +80,14 @@ def test_gpu_large_k_and_trajectory():
             assert np.array_equal(dev.traj[t0:t0 + n], orc["traj"][t0:t0 + n]), j
 
 
-def test_gpu_trajectory_matches_reference():
+@pytest.mark.parametrize("algo", [1, 2])
+def test_gpu_trajectory_matches_reference(algo):
     d = load_corpus("random_34")
     lens = d["P_traj_len"]
     starts = np.concatenate([[0], np.cumsum(lens)])
     for ladder, ids in groups(d).items():
         b = sub_batch(d, ids)
-        res = search.solve_batch(b, ladder=ladder, collect_trajectory=True)
+        res = search.solve_batch(b, ladder=ladder, collect_trajectory=True, algorithm=algo)
         for j, i in enumerate(ids):
             t0 = int(res.traj_offsets[j])
             got = res.traj[t0:t0 + int(res.traj_len[j])]
@@ -112,9 +118,10 @@ def test_gpu_k64_three_classes_deep_search():
     """K = 64 with three classes: thousands of dfs calls per instance."""
     batch, ladders = random_batch(98, 8, k_min=60, k_max=64, max_classes=3)
     for lad, (idx, sb) in group_by_ladder(batch, ladders).items():
-        dev = search.solve_batch(sb, ladder=lad)
-        orc = oracle.dftsp_batch(sb, ladder=lad, threads=8)
-        _assert_same(dev, orc, sb, f"K=64 ladder {lad}")
+        for algo in (1, 2):
+            dev = search.solve_batch(sb, ladder=lad, algorithm=algo)
+            orc = oracle.dftsp_batch(sb, ladder=lad, threads=8)
+            _assert_same(dev, orc, sb, f"K=64 ladder {lad} algo {algo}")
 
 
 def test_gpu_edge_statuses():
@@ -136,3 +143,21 @@ def test_gpu_edge_statuses():
     assert np.array_equal(dev.status, orc["status"])
     assert np.array_equal(dev.error_index, orc["error_index"])
     _assert_same(dev, orc, b, "edge statuses")
+
+
+def test_gpu_v2_table_overflow_falls_back_exactly():
+    """Many classes with many members: u32 leaf counts overflow, the instance
+    is re-run by the literal walk and still matches the oracle."""
+    batch, _ = random_batch(97, 4, k_min=56, k_max=56, max_classes=5)
+    rng = np.random.default_rng(2)
+    batch.columns["output_tokens"][:] = rng.choice(np.arange(1, 15) * 8, size=batch.n_req)
+    batch.columns["deadline_s"][:] = 1e6
+    batch.columns["channel_gain"][:] = 1.0
+    for c in batch.contexts:
+        c["memory_bytes"] *= 1e6
+        c["flops_per_s"] *= 1e6
+        c["uplink_band_hz"] = c["downlink_band_hz"] = 1e9
+        c["has_slot_cap"] = 0
+    dev = search.solve_batch(batch, ladder=None, algorithm=2)
+    orc = oracle.dftsp_batch(batch, ladder=None, threads=4)
+    _assert_same(dev, orc, batch, "overflow fallback")
