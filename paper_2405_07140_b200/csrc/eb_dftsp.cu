@@ -1168,6 +1168,7 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   DftspArgs A;
   A.ctxs = d_ctxs; A.n_ctx = n_ctx; A.prm = prm; A.n_inst = n_inst; A.offsets = d_off;
   A.ctx_index = d_ctx_index; A.req_base = req_base; A.req = d_req; A.K = K; A.G = G;
+  A.out = d_out; A.traj_base = traj_base; A.counter = d_counter; A.fallback_pass = 0;
   // algorithm: 2 = leaf-parallel (default) unless its tables do not fit two
   // warps per block, 1 = literal lanes-per-call (also v2's in-kernel fallback)
   int algo = prm.algorithm;
