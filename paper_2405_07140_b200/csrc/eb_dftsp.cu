@@ -69,7 +69,8 @@ __host__ __device__ inline Lay make_lay(int K, int G, bool exact, bool v2) {
   L.T = K * (K + 1) / 2 + K * G;
   L.t_up = take(8 * (size_t)L.T); L.t_dn = take(8 * (size_t)L.T);
   L.t_tau = exact ? take(8 * (size_t)L.T) : 0;
-  L.ring_v = take(8 * RING); L.ring_p = take(8 * RING); L.ring_done = take(RING);
+  if (!v2) { L.ring_v = take(8 * RING); L.ring_p = take(8 * RING); L.ring_done = take(RING); }
+  else { L.ring_v = L.ring_p = L.ring_done = 0; }
   L.sol = take(K);
   if (v2) {
     const int lvls = G > 1 ? G - 1 : 1;
@@ -294,6 +295,32 @@ __device__ __forceinline__ void warp_prefix2(int n, ValFn val, StoreFn store) {
   }
 }
 
+// Single-sequence version of warp_prefix2.
+template <typename ValFn, typename StoreFn>
+__device__ __forceinline__ void warp_prefix1(int n, ValFn val, StoreFn store) {
+  const int lane = threadIdx.x & 31;
+  const int q = (n + 32) >> 5;
+  uint64_t va[3], la = 0;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    int r = lane * q + j;
+    va[j] = (j < q && r <= n) ? val(r) : 0;
+    la += va[j];
+  }
+  uint64_t ia = la;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t ta = __shfl_up_sync(EB_FULL, ia, o);
+    if (lane >= o) ia += ta;
+  }
+  uint64_t ra = ia - la;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    int r = lane * q + j;
+    if (j < q && r <= n) { ra += va[j]; store(r, ra); }
+  }
+}
+
 // Full-traversal node counts of one dfs level (dftsp.py:183-234) entered at
 // level k with remaining target r >= 1: (visited, pruned).  PF* = prefix
 // sums over r of F(k+1, .) (index r, F(., 0) = 0).
@@ -338,12 +365,13 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
   const int LV = Gi > 1 ? Gi - 1 : 1;
   const int W = n + 2;
 
-  // ---- U: unranking tables.  For partition d and level k >= 1,
+  // ---- U: unranking tables, built lazily for pool widths d that have a
+  //      call surviving the skip test.  For level k >= 1 of partition d,
   //      PQ_k[x + 1] = #{(c_k..c_{m-1}) : bounds, sum <= x}  (prefix of Q_k).
-  bool ovf = false;
-  for (int d = 1; d <= n; ++d) {
+  uint64_t built = 0;       // bit d-1: tables of width d are ready
+  auto build_pq = [&](int d) -> bool {
     const int m = ncls_d[d - 1];
-    if (m < 2) continue;
+    if (m < 2) return true;
     const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
     uint32_t* base = pq + (size_t)(d - 1) * LV * W;
     {
@@ -352,18 +380,18 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
       for (int x = lane; x <= n + 1; x += 32) P[x] = (x == 0) ? 0u : (uint32_t)(min(x - 1, sl) + 1);
     }
     __syncwarp();
+    bool ovf = false;
     for (int k = m - 2; k >= 1; --k) {
       const uint32_t* Pn = base + (size_t)k * W;        // level k+1
       uint32_t* Pk = base + (size_t)(k - 1) * W;        // level k
       const int sk = row[k].size;
       bool o2 = false;
-      warp_prefix2(n,
-          [&](int r, uint64_t& a, uint64_t& b) {
+      warp_prefix1(n,
+          [&](int r) -> uint64_t {
             int lo = r - sk - 1;
-            a = (uint64_t)Pn[r + 1] - (lo >= 0 ? (uint64_t)Pn[lo + 1] : 0);
-            b = 0;
+            return (uint64_t)Pn[r + 1] - (lo >= 0 ? (uint64_t)Pn[lo + 1] : 0);
           },
-          [&](int r, uint64_t a, uint64_t) {
+          [&](int r, uint64_t a) {
             if (a > 0x7fffffffULL) o2 = true;
             Pk[r + 1] = (uint32_t)a;
           });
@@ -371,8 +399,8 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
       ovf |= __any_sync(EB_FULL, o2);
       __syncwarp();
     }
-  }
-  if (ovf) return false;
+    return !ovf;
+  };
 
   // ---- S: leaves in sequence order (z from n down, d from z up, lex-desc)
   found = false;
@@ -382,20 +410,13 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
     const double mem_cap = sub(k2, i2d((int64_t)padded * z));      // mem_budget(z)
     const int nd = n - z + 1;
     uint32_t cnt[2] = {0, 0};
+    bool live[2] = {false, false};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int d = z + lane + 32 * h;
       if (d > n) continue;
       const int m = ncls_d[d - 1];
       const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
-      uint32_t N;
-      if (m == 1) {
-        N = (z <= row[0].size) ? 1u : 0u;
-      } else {
-        const uint32_t* P1 = pq + (size_t)(d - 1) * LV * W;        // level 1
-        const int hi0 = min(z, (int)row[0].size), lo0 = max(0, z - (int)row[0].tail_next);
-        N = (hi0 >= lo0) ? P1[z - lo0 + 1] - P1[z - hi0] : 0u;
-      }
       // sound skip: greedy (first) leaf fails memory or latency by a margin
       int rem = z;
       int64_t mem = 0;
@@ -408,8 +429,34 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
         rem -= c;
       }
       const double lat_cap = EXACT ? slot_cap : pymin(sub(o_tau[d - 1], k3z), slot_cap);
-      const bool skip = fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap);
-      cnt[h] = skip ? 0u : N;
+      live[h] = !(fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap));
+    }
+    // unranking tables for the surviving widths (once per width)
+    {
+      uint64_t want = ((uint64_t)__ballot_sync(EB_FULL, live[0]) << (z - 1)) |
+                      (nd > 32 ? ((uint64_t)__ballot_sync(EB_FULL, live[1]) << (z + 31)) : 0);
+      want &= ~built;
+      bool ok = true;
+      while (want) {
+        const int d = __ffsll((long long)want);
+        want &= want - 1;
+        ok &= build_pq(d);
+        built |= 1ULL << (d - 1);
+      }
+      if (!ok) return false;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int d = z + lane + 32 * h;
+      if (d > n || !live[h]) continue;
+      const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
+      if (ncls_d[d - 1] == 1) {
+        cnt[h] = (z <= row[0].size) ? 1u : 0u;
+      } else {
+        const uint32_t* P1 = pq + (size_t)(d - 1) * LV * W;        // level 1
+        const int hi0 = min(z, (int)row[0].size), lo0 = max(0, z - (int)row[0].tail_next);
+        cnt[h] = (hi0 >= lo0) ? P1[z - lo0 + 1] - P1[z - hi0] : 0u;
+      }
     }
     // exclusive prefix of cnt over d = z..n (lane order, then +32)
     uint32_t inc0 = cnt[0], inc1 = cnt[1];
@@ -490,10 +537,22 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
   // ---- C: node counts.  Calls (z, d) counted: z > zf (all d >= z), and
   //      z == zf with d < dwin; plus the winner's partial count.
   uint64_t my_v = 0, my_p = 0;
+  int prev_m = -1;
+  const LevelInfo* prev_row = lvl;
   for (int d = found ? zf : 1; d <= n; ++d) {
     const int m = ncls_d[d - 1];
     const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
-    for (int k = m - 1; k >= 1; --k) {
+    // F(k, .) depends only on levels k..m-1; consecutive widths differ in one
+    // class size (and the tails above it), so deeper levels are reused.
+    int kc = m - 1;
+    if (m == prev_m) {
+      kc = 0;
+      for (int k = m - 1; k >= 1; --k)
+        if (row[k].size != prev_row[k].size || row[k].tail_next != prev_row[k].tail_next) { kc = k; break; }
+    }
+    prev_m = m;
+    prev_row = row;
+    for (int k = kc; k >= 1; --k) {
       const uint64_t* NV = pfv + (size_t)(k + 1) * (n + 1);
       const uint64_t* NP = pfp + (size_t)(k + 1) * (n + 1);
       uint64_t* KV = pfv + (size_t)k * (n + 1);
@@ -559,7 +618,7 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
   return true;
 }
 
-template <bool PRUNE, bool INCL, bool EXACT, int ALGO>
+template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI>
 __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* smem) {
   const int lane = threadIdx.x & 31;
   const int K = A.K, G = A.G;
@@ -626,12 +685,12 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   const Ctx C = load_ctx(&A.ctxs[ci]);
 
   // ---------------- setup: per request (lanes over i = lane, lane+32) -----
-  int s_i[2], len_i[2];
-  int64_t id_i[2];
-  double dl_i[2], w_i[2], g_i[2], p_i[2];
+  int s_i[NI], len_i[NI];
+  int64_t id_i[NI];
+  double dl_i[NI], w_i[NI], g_i[NI], p_i[NI];
   int padded = 0;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NI; ++h) {
     int i = lane + 32 * h;
     if (i < n) {
       int64_t r = r0 + i;
@@ -652,7 +711,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   // Duplicate ids (coefficients are keyed by id, feasibility.py:164-166).
   int err_dup = INT_MAX;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NI; ++h) {
     int i = lane + 32 * h;
     if (i < n)
       for (int j = 0; j < i; ++j)
@@ -674,10 +733,10 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   const double k5 = i2d(2 * C.m.L * C.m.d);
   const double slot_base = C.has_cap ? div(mul(C.cap_s, C.C), C.beta) : 0.0;  // feasibility.py:124
 
-  double key_i[2], dnt_i[2], tau_i[2];
+  double key_i[NI], dnt_i[NI], tau_i[NI];
   int err_link = INT_MAX, err_code = 0;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NI; ++h) {
     int i = lane + 32 * h;
     key_i[h] = dnt_i[h] = tau_i[h] = 0.0;
     if (i < n) {
@@ -708,10 +767,10 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
 
   // order = sorted by (-tau_base, id) (dftsp.py:257); classes by ascending
   // output length with within-class order (key, id) (dftsp.py:71-82).
-  int t_i[2], gcls_i[2], kr_i[2];
-  bool first_i[2];
+  int t_i[NI], gcls_i[NI], kr_i[NI];
+  bool first_i[NI];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NI; ++h) {
     int i = lane + 32 * h;
     t_i[h] = gcls_i[h] = kr_i[h] = 0;
     first_i[h] = false;
@@ -730,7 +789,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   // class index = number of distinct lengths below mine
   unsigned long long firstmask = 0;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NI; ++h) {
     unsigned b = __ballot_sync(EB_FULL, first_i[h]);
     firstmask |= (unsigned long long)b << (32 * h);
   }
@@ -740,7 +799,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   int bad_t = INT_MAX, bad_i = -1;
   if (A.prm.ladder_len > 0) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < NI; ++h) {
       int i = lane + 32 * h;
       if (i < n) {
         bool ok = false;
@@ -759,7 +818,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     }
   }
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NI; ++h) {
     int i = lane + 32 * h;
     if (i < n) {
       int g = 0, kr = 0;
@@ -795,7 +854,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   if (lane < Gi) c_cnt[lane] = 0;
   __syncwarp();
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NI; ++h) {
     int i = lane + 32 * h;
     if (i < n) atomicAdd(&c_cnt[gcls_i[h]], 1);
   }
@@ -807,7 +866,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   }
   __syncwarp();
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NI; ++h) {
     int i = lane + 32 * h;
     if (i < n) c_list[c_start[gcls_i[h]] + kr_i[h]] = (uint8_t)t_i[h];
   }
@@ -865,7 +924,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       }
     }
   }
-  if (lane < RING / 32 * 32) { ring_done[lane] = 0; ring_done[lane + 32] = 0; }
+  if constexpr (ALGO == 1) { ring_done[lane] = 0; ring_done[lane + 32] = 0; }
   __syncwarp();
 
   // ---------------- search ------------------------------------------------
@@ -1062,8 +1121,8 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   }
 }
 
-template <bool PRUNE, bool INCL, bool EXACT, int ALGO>
-__global__ void __launch_bounds__(128) dftsp_kernel(DftspArgs A) {
+template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI>
+__global__ void __launch_bounds__(128, 4) dftsp_kernel(DftspArgs A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   const int warp = threadIdx.x >> 5;
   unsigned char* smem = smem_all + warp * A.warp_bytes;
@@ -1076,7 +1135,7 @@ __global__ void __launch_bounds__(128) dftsp_kernel(DftspArgs A) {
     inst = __shfl_sync(EB_FULL, inst, 0);
     if (inst >= A.n_inst) break;
     if (A.fallback_pass && A.out.status[inst] != EB_STATUS_FALLBACK) continue;
-    solve_instance<PRUNE, INCL, EXACT, ALGO>(A, inst, smem);
+    solve_instance<PRUNE, INCL, EXACT, ALGO, NI>(A, inst, smem);
     __syncwarp();
   }
 }
@@ -1182,14 +1241,15 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   size_t smem = A.warp_bytes * warps;
   void (*kern)(DftspArgs);
   const bool P = prm.pruning != 0, I = prm.inclusive_bound != 0;
-#define EB_PICK(AL)                                                                              \
-  if (P) {                                                                                       \
-    if (I) kern = exact ? dftsp_kernel<true, true, true, AL> : dftsp_kernel<true, true, false, AL>; \
-    else kern = exact ? dftsp_kernel<true, false, true, AL> : dftsp_kernel<true, false, false, AL>; \
-  } else {                                                                                       \
-    if (I) kern = exact ? dftsp_kernel<false, true, true, AL> : dftsp_kernel<false, true, false, AL>; \
-    else kern = exact ? dftsp_kernel<false, false, true, AL> : dftsp_kernel<false, false, false, AL>; \
+#define EB_PICK3(AL, NI)                                                                           \
+  if (P) {                                                                                         \
+    if (I) kern = exact ? dftsp_kernel<true, true, true, AL, NI> : dftsp_kernel<true, true, false, AL, NI>;   \
+    else kern = exact ? dftsp_kernel<true, false, true, AL, NI> : dftsp_kernel<true, false, false, AL, NI>;   \
+  } else {                                                                                         \
+    if (I) kern = exact ? dftsp_kernel<false, true, true, AL, NI> : dftsp_kernel<false, true, false, AL, NI>; \
+    else kern = exact ? dftsp_kernel<false, false, true, AL, NI> : dftsp_kernel<false, false, false, AL, NI>; \
   }
+#define EB_PICK(AL) if (K <= 32) { EB_PICK3(AL, 1) } else { EB_PICK3(AL, 2) }
   if (algo == 2) { EB_PICK(2) } else { EB_PICK(1) }
   A.fallback_pass = 0;
   EB_CUDA(cudaMemsetAsync(d_counter, 0, 2 * sizeof(int), st));
@@ -1205,6 +1265,7 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   EB_CUDA(cudaMemsetAsync(d_counter, 0, sizeof(int), st));
   int rc2 = launch_one(h, st, kern, B, wb, B.warp_bytes * wb, n_inst);
 #undef EB_PICK
+#undef EB_PICK3
   return rc2;
 }
 
