@@ -181,7 +181,10 @@ def main():
 
     d_off = to_dev(batch.offsets)
     d_ci = to_dev(batch.ctx_index)
-    d_cols = {k: to_dev(v) for k, v in batch.columns.items()}
+    # dftsp reads every request column except `tolerance` (candidates are
+    # already accuracy-admitted, sim.py:264-274), so it is not shipped
+    used = [k for k in batch.columns if k != "tolerance"]
+    d_cols = {k: to_dev(batch.columns[k]) for k in used}
     d_ctx = to_dev(batch.contexts.view(np.uint8)).contiguous()
     outs = {"status": torch.zeros(n, dtype=torch.int32, device=dev),
             "error_index": torch.zeros(n, dtype=torch.int32, device=dev),
@@ -241,7 +244,7 @@ def main():
     # ---- e2e through the C ABI with pinned host buffers --------------------
     e2e = None
     if not args.no_e2e:
-        pin = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in batch.columns.items()}
+        pin = {k: torch.from_numpy(np.ascontiguousarray(batch.columns[k])).pin_memory() for k in used}
         p_off = torch.from_numpy(batch.offsets).pin_memory()
         p_ci = torch.from_numpy(batch.ctx_index).pin_memory()
         hout = {"status": torch.zeros(n, dtype=torch.int32).pin_memory(),

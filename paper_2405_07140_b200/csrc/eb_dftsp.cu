@@ -75,7 +75,7 @@ __host__ __device__ inline Lay make_lay(int K, int G, bool exact, bool v2) {
   if (v2) {
     const int lvls = G > 1 ? G - 1 : 1;
     L.pq = take(4 * (size_t)K * lvls * (K + 2));
-    L.pre = take(4 * (size_t)(K + 2));
+    L.pre = take(4 * 64);
     L.pf = take(16 * (size_t)G * (K + 1));
   } else {
     L.pq = L.pre = L.pf = 0;
@@ -268,13 +268,13 @@ __device__ __forceinline__ bool fails_with_margin(double a_lo, double b) {
 }
 
 // Blocked warp-wide inclusive prefix over r = 0..n of two u64 sequences.
-template <typename ValFn, typename StoreFn>
+template <int QMAX, typename ValFn, typename StoreFn>
 __device__ __forceinline__ void warp_prefix2(int n, ValFn val, StoreFn store) {
   const int lane = threadIdx.x & 31;
-  const int q = (n + 32) >> 5;                 // ceil((n + 1) / 32) <= 3
-  uint64_t va[3], vb[3], la = 0, lb = 0;
+  const int q = (n + 32) >> 5;                 // ceil((n + 1) / 32) <= QMAX
+  uint64_t va[QMAX], vb[QMAX], la = 0, lb = 0;
 #pragma unroll
-  for (int j = 0; j < 3; ++j) {
+  for (int j = 0; j < QMAX; ++j) {
     int r = lane * q + j;
     va[j] = vb[j] = 0;
     if (j < q && r <= n) val(r, va[j], vb[j]);
@@ -289,20 +289,20 @@ __device__ __forceinline__ void warp_prefix2(int n, ValFn val, StoreFn store) {
   }
   uint64_t ra = ia - la, rb = ib - lb;
 #pragma unroll
-  for (int j = 0; j < 3; ++j) {
+  for (int j = 0; j < QMAX; ++j) {
     int r = lane * q + j;
     if (j < q && r <= n) { ra += va[j]; rb += vb[j]; store(r, ra, rb); }
   }
 }
 
 // Single-sequence version of warp_prefix2.
-template <typename ValFn, typename StoreFn>
+template <int QMAX, typename ValFn, typename StoreFn>
 __device__ __forceinline__ void warp_prefix1(int n, ValFn val, StoreFn store) {
   const int lane = threadIdx.x & 31;
   const int q = (n + 32) >> 5;
-  uint64_t va[3], la = 0;
+  uint64_t va[QMAX], la = 0;
 #pragma unroll
-  for (int j = 0; j < 3; ++j) {
+  for (int j = 0; j < QMAX; ++j) {
     int r = lane * q + j;
     va[j] = (j < q && r <= n) ? val(r) : 0;
     la += va[j];
@@ -315,7 +315,7 @@ __device__ __forceinline__ void warp_prefix1(int n, ValFn val, StoreFn store) {
   }
   uint64_t ra = ia - la;
 #pragma unroll
-  for (int j = 0; j < 3; ++j) {
+  for (int j = 0; j < QMAX; ++j) {
     int r = lane * q + j;
     if (j < q && r <= n) { ra += va[j]; store(r, ra); }
   }
@@ -349,7 +349,7 @@ __device__ __forceinline__ void level_counts(const LevelInfo& li, bool last, int
   }
 }
 
-template <bool PRUNE, bool INCL, bool EXACT>
+template <bool PRUNE, bool INCL, bool EXACT, int NI>
 __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, const LevelInfo* lvl,
                           const uint8_t* ncls_d, const double* t_up, const double* t_dn, const double* t_tau,
                           const int32_t* c_len, const double* c_w, const double* o_tau, double k2, double k3,
@@ -386,7 +386,7 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
       uint32_t* Pk = base + (size_t)(k - 1) * W;        // level k
       const int sk = row[k].size;
       bool o2 = false;
-      warp_prefix1(n,
+      warp_prefix1<NI + 1>(n,
           [&](int r) -> uint64_t {
             int lo = r - sk - 1;
             return (uint64_t)Pn[r + 1] - (lo >= 0 ? (uint64_t)Pn[lo + 1] : 0);
@@ -402,99 +402,102 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
     return !ovf;
   };
 
-  // ---- S: leaves in sequence order (z from n down, d from z up, lex-desc)
+  // ---- S: the call sequence (z from n down, d from z up) in windows of 32
+  //      calls, lane = call: skip test, then the surviving calls' leaves in
+  //      sequence order, 32 per step, first passing leaf wins.
   found = false;
-  for (int z = n; z >= 1 && !found; --z) {
-    const double k3z = mul(k3, i2d(z));                            // coeff.k3 * z
-    const double slot_cap = has_cap ? sub(slot_base, k3z) : INF;  // slot_budget(z)
-    const double mem_cap = sub(k2, i2d((int64_t)padded * z));      // mem_budget(z)
-    const int nd = n - z + 1;
-    uint32_t cnt[2] = {0, 0};
-    bool live[2] = {false, false};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int d = z + lane + 32 * h;
-      if (d > n) continue;
+  const int total_calls = n * (n + 1) / 2;
+  for (int c0 = 0; c0 < total_calls && !found; c0 += 32) {
+    const int c = c0 + lane;
+    int z = 0, d = 0;
+    bool live = false;
+    if (c < total_calls) {
+      call_zd(n, c, z, d);
+      const double k3z = mul(k3, i2d(z));                            // coeff.k3 * z
+      const double slot_cap = has_cap ? sub(slot_base, k3z) : INF;  // slot_budget(z)
+      const double mem_cap = sub(k2, i2d((int64_t)padded * z));      // mem_budget(z)
       const int m = ncls_d[d - 1];
       const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
       // sound skip: greedy (first) leaf fails memory or latency by a margin
       int rem = z;
       int64_t mem = 0;
       double lat = 0.0;
-      for (int k = 0; k < m; ++k) {
+      for (int k = 0; k < m && rem > 0; ++k) {
         const LevelInfo li = row[k];
-        const int c = min(rem, (int)li.size);
-        mem += (int64_t)c * c_len[li.g];
-        lat = add(lat, mul(i2d(c), c_w[li.g]));
-        rem -= c;
+        const int cc = min(rem, (int)li.size);
+        mem += (int64_t)cc * c_len[li.g];
+        lat = add(lat, mul(i2d(cc), c_w[li.g]));
+        rem -= cc;
       }
       const double lat_cap = EXACT ? slot_cap : pymin(sub(o_tau[d - 1], k3z), slot_cap);
-      live[h] = !(fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap));
+      live = !(fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap));
     }
-    // unranking tables for the surviving widths (once per width)
+    // unranking tables for surviving widths (once per width)
     {
-      uint64_t want = ((uint64_t)__ballot_sync(EB_FULL, live[0]) << (z - 1)) |
-                      (nd > 32 ? ((uint64_t)__ballot_sync(EB_FULL, live[1]) << (z + 31)) : 0);
+      const uint64_t bit = live ? (1ULL << (d - 1)) : 0ULL;
+      uint64_t want = (uint64_t)__reduce_or_sync(EB_FULL, (unsigned)bit) |
+                      ((uint64_t)__reduce_or_sync(EB_FULL, (unsigned)(bit >> 32)) << 32);
       want &= ~built;
       bool ok = true;
       while (want) {
-        const int d = __ffsll((long long)want);
+        const int dd = __ffsll((long long)want);
         want &= want - 1;
-        ok &= build_pq(d);
-        built |= 1ULL << (d - 1);
+        ok &= build_pq(dd);
+        built |= 1ULL << (dd - 1);
       }
       if (!ok) return false;
     }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int d = z + lane + 32 * h;
-      if (d > n || !live[h]) continue;
+    uint32_t cnt = 0;
+    if (live) {
       const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
       if (ncls_d[d - 1] == 1) {
-        cnt[h] = (z <= row[0].size) ? 1u : 0u;
+        cnt = (z <= row[0].size) ? 1u : 0u;
       } else {
         const uint32_t* P1 = pq + (size_t)(d - 1) * LV * W;        // level 1
         const int hi0 = min(z, (int)row[0].size), lo0 = max(0, z - (int)row[0].tail_next);
-        cnt[h] = (hi0 >= lo0) ? P1[z - lo0 + 1] - P1[z - hi0] : 0u;
+        cnt = (hi0 >= lo0) ? P1[z - lo0 + 1] - P1[z - hi0] : 0u;
       }
     }
-    // exclusive prefix of cnt over d = z..n (lane order, then +32)
-    uint32_t inc0 = cnt[0], inc1 = cnt[1];
+    uint32_t inc = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      uint32_t t0 = __shfl_up_sync(EB_FULL, inc0, o), t1 = __shfl_up_sync(EB_FULL, inc1, o);
-      if (lane >= o) { inc0 += t0; inc1 += t1; }
+      uint32_t t = __shfl_up_sync(EB_FULL, inc, o);
+      if (lane >= o) inc += t;
     }
-    const uint32_t tot0 = __shfl_sync(EB_FULL, inc0, 31);
-    inc1 += tot0;
-    const uint32_t T = __shfl_sync(EB_FULL, inc1, 31);
-    if (lane < nd) pre[lane] = inc0 - cnt[0];
-    if (lane + 32 < nd) pre[lane + 32] = inc1 - cnt[1];
+    const uint32_t T = __shfl_sync(EB_FULL, inc, 31);
+    if (T == 0) continue;
+    pre[lane] = inc - cnt;
+    pre[32 + lane] = (uint32_t)((z << 8) | d);                      // call of this slot
     __syncwarp();
     for (uint32_t b0 = 0; b0 < T; b0 += 32) {
       const uint32_t g = b0 + lane;
       bool pass = false;
-      int d = 0, klast = 0;
+      int klast = 0, zz = 0, dd = 0;
       uint64_t V0 = 0, V1 = 0;
       if (g < T) {
-        int a = 0, bnd = nd - 1;                                   // largest idx with pre[idx] <= g
+        int a = 0, bnd = 31;                                       // largest slot with pre[slot] <= g
         while (a < bnd) {
           int mid = (a + bnd + 1) >> 1;
           if (pre[mid] <= g) a = mid; else bnd = mid - 1;
         }
-        d = z + a;
+        const uint32_t zd = pre[32 + a];
+        zz = (int)(zd >> 8);
+        dd = (int)(zd & 0xff);
         uint32_t i = g - pre[a];
-        const int m = ncls_d[d - 1];
-        const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
-        const uint32_t* base = pq + (size_t)(d - 1) * LV * W;
-        int r = z;
+        const double k3z = mul(k3, i2d(zz));
+        const double slot_cap = has_cap ? sub(slot_base, k3z) : INF;
+        const double mem_cap = sub(k2, i2d((int64_t)padded * zz));
+        const int m = ncls_d[dd - 1];
+        const LevelInfo* row = lvl + (size_t)(dd - 1) * Gi;
+        const uint32_t* base = pq + (size_t)(dd - 1) * LV * W;
+        int r = zz;
         double u = 0.0, dl = 0.0, lat = 0.0, tau = INF;
         int64_t mem = 0;
         for (int k = 0; k < m; ++k) {
           const LevelInfo li = row[k];
-          int c;
+          int cc;
           if (k == m - 1) {
-            c = r;
+            cc = r;
           } else {                                                 // unrank level k
             const uint32_t* P = base + (size_t)k * W;              // level k+1 prefix
             const int hi = min(r, (int)li.size), lo = max(0, r - (int)li.tail_next);
@@ -505,25 +508,25 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
               if (P[mid + 1] - pb > i) xz = mid; else xa = mid + 1;
             }
             i -= P[xa] - pb;
-            c = r - xa;
+            cc = r - xa;
           }
-          if (c) { setV(V0, V1, k, c); klast = k; }
-          u = add(u, t_up[li.off + c]);                            // up_acc + up[k][x]
-          dl = add(dl, t_dn[li.off + c]);
-          mem += (int64_t)c * c_len[li.g];
-          lat = add(lat, mul(i2d(c), c_w[li.g]));
-          if (EXACT && c) tau = pymin(tau, t_tau[li.off + c]);
-          r -= c;
+          if (cc) { setV(V0, V1, k, cc); klast = k; }
+          u = add(u, t_up[li.off + cc]);                           // up_acc + up[k][x]
+          dl = add(dl, t_dn[li.off + cc]);
+          mem += (int64_t)cc * c_len[li.g];
+          lat = add(lat, mul(i2d(cc), c_w[li.g]));
+          if (EXACT && cc) tau = pymin(tau, t_tau[li.off + cc]);
+          r -= cc;
         }
-        const double cap = EXACT ? pymin(sub(tau, k3z), slot_cap) : pymin(sub(o_tau[d - 1], k3z), slot_cap);
+        const double cap = EXACT ? pymin(sub(tau, k3z), slot_cap) : pymin(sub(o_tau[dd - 1], k3z), slot_cap);
         pass = leq(u, 1.0) && leq(dl, 1.0) && leq(i2d(mem), mem_cap) && leq(lat, cap);
       }
       const unsigned bal = __ballot_sync(EB_FULL, pass);
       if (bal) {
         const int src = __ffs(bal) - 1;
         found = true;
-        zf = z;
-        dwin = __shfl_sync(EB_FULL, d, src);
+        zf = __shfl_sync(EB_FULL, zz, src);
+        dwin = __shfl_sync(EB_FULL, dd, src);
         kwin = __shfl_sync(EB_FULL, klast, src);
         W0 = __shfl_sync(EB_FULL, V0, src);
         W1 = __shfl_sync(EB_FULL, V1, src);
@@ -559,7 +562,7 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
       uint64_t* KP = pfp + (size_t)k * (n + 1);
       const LevelInfo li = row[k];
       const bool last = (k == m - 1);
-      warp_prefix2(n,
+      warp_prefix2<NI + 1>(n,
           [&](int r, uint64_t& a, uint64_t& b) {
             if (r == 0) { a = b = 0; return; }
             level_counts<PRUNE, INCL>(li, last, r, NV, NP, a, b);
@@ -618,6 +621,29 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
   return true;
 }
 
+// Error / empty exit of one instance (kept out of line: one copy serves
+// every early-exit site, which keeps the kernel's instruction footprint small).
+__device__ __noinline__ void write_status(const eb_dftsp_result& O, int64_t inst, int64_t r0, int n, int st,
+                                          int err) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    O.status[inst] = st;
+    if (O.error_index) O.error_index[inst] = err;
+    O.z_found[inst] = 0;
+    O.nodes_visited[inst] = 0;
+    O.nodes_pruned[inst] = 0;
+    if (O.n_classes) O.n_classes[inst] = 0;
+    if (O.traj_len) O.traj_len[inst] = 0;
+  }
+  if (O.metrics && lane < EB_N_METRICS) O.metrics[inst * EB_N_METRICS + lane] = 0.0;
+  if (lane < EB_MAX_CLASSES) {
+    if (O.counts) O.counts[inst * EB_MAX_CLASSES + lane] = 0;
+    if (O.class_lengths) O.class_lengths[inst * EB_MAX_CLASSES + lane] = 0;
+  }
+  if (O.solution)
+    for (int j = lane; j < n; j += 32) O.solution[r0 + j] = -1;
+}
+
 template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI>
 __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* smem) {
   const int lane = threadIdx.x & 31;
@@ -659,24 +685,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   const int n = (int)(A.offsets[inst + 1] - row0);
   const int64_t r0 = row0 - A.req_base;
 
-  auto put_status = [&](int st, int err) {
-    if (lane == 0) {
-      O.status[inst] = st;
-      if (O.error_index) O.error_index[inst] = err;
-      O.z_found[inst] = 0;
-      O.nodes_visited[inst] = 0;
-      O.nodes_pruned[inst] = 0;
-      if (O.n_classes) O.n_classes[inst] = 0;
-      if (O.traj_len) O.traj_len[inst] = 0;
-    }
-    if (O.metrics && lane < EB_N_METRICS) O.metrics[inst * EB_N_METRICS + lane] = 0.0;
-    if (lane < EB_MAX_CLASSES) {
-      if (O.counts) O.counts[inst * EB_MAX_CLASSES + lane] = 0;
-      if (O.class_lengths) O.class_lengths[inst * EB_MAX_CLASSES + lane] = 0;
-    }
-    if (O.solution)
-      for (int j = lane; j < n; j += 32) O.solution[r0 + j] = -1;
-  };
+  auto put_status = [&](int st, int err) { write_status(O, inst, r0, n, st, err); };
 
   int ci = A.ctx_index ? A.ctx_index[inst] : 0;
   if (ci < 0 || ci >= A.n_ctx) { put_status(EB_ERR_INVALID_ARG, -1); return; }
@@ -937,7 +946,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   int zf = 0, dwin = 0, kwin = 0;
   uint64_t W0 = 0, W1 = 0;
   if constexpr (ALGO == 2) {
-    if (!search_v2<PRUNE, INCL, EXACT>(n, Gi, smem, L, lvl, ncls_d, t_up, t_dn, t_tau, c_len, c_w, o_tau, k2, k3,
+    if (!search_v2<PRUNE, INCL, EXACT, NI>(n, Gi, smem, L, lvl, ncls_d, t_up, t_dn, t_tau, c_len, c_w, o_tau, k2, k3,
                                        slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
                                        tot_v, tot_p)) {
       // leaf counts overflow the u32 unranking tables: hand the instance to

@@ -13,8 +13,11 @@
 
 #if defined(__CUDACC__)
 #define EB_HD __host__ __device__ __forceinline__
+// out of line on the device: a bulky routine called a few times per instance
+#define EB_HD_OUTLINE static __host__ __device__ __noinline__
 #else
 #define EB_HD static inline
+#define EB_HD_OUTLINE static inline
 #endif
 
 #if defined(__CUDA_ARCH__)
@@ -113,7 +116,7 @@ EB_HD bool leq(double a, double b) {
 // objdump: see tools/gen_log2_table.py).  Bit-identical to the host libm on
 // every input, which tests/test_log2.py checks on >10^7 inputs.
 // ---------------------------------------------------------------------------
-EB_HD double log2_glibc(double x) {
+EB_HD_OUTLINE double log2_glibc(double x) {
   const double InvLn2hi = EB_LOG2_INVLN2HI;
   const double InvLn2lo = EB_LOG2_INVLN2LO;
   uint64_t ix = as_u64(x);
