@@ -349,8 +349,17 @@ __device__ __forceinline__ void level_counts(const LevelInfo& li, bool last, int
   }
 }
 
+// Phase barrier of the lockstep (ALGO 2) kernel: every warp of the block
+// passes the same three barriers per instance round, so the SM executes one
+// phase's code at a time (instruction-cache locality).
+template <int ALGO>
+__device__ __forceinline__ void phase_barrier(int& passed) {
+  if constexpr (ALGO == 2) __syncthreads();
+  ++passed;
+}
+
 template <bool PRUNE, bool INCL, bool EXACT, int NI>
-__device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, const LevelInfo* lvl,
+__device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const Lay& L, const LevelInfo* lvl,
                           const uint8_t* ncls_d, const double* t_up, const double* t_dn, const double* t_tau,
                           const int32_t* c_len, const double* c_w, const double* o_tau, double k2, double k3,
                           double slot_base, bool has_cap, int padded, int64_t* traj, bool& found, int& zf,
@@ -537,6 +546,7 @@ __device__ bool search_v2(int n, int Gi, unsigned char* smem, const Lay& L, cons
   }
   best = found ? (n - zf) * (n - zf + 1) / 2 + (dwin - zf) : INT_MAX;
 
+  phase_barrier<2>(passed);
   // ---- C: node counts.  Calls (z, d) counted: z > zf (all d >= z), and
   //      z == zf with d < dwin; plus the winner's partial count.
   uint64_t my_v = 0, my_p = 0;
@@ -645,7 +655,7 @@ __device__ __noinline__ void write_status(const eb_dftsp_result& O, int64_t inst
 }
 
 template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI>
-__device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* smem) {
+__device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* smem, int& passed) {
   const int lane = threadIdx.x & 31;
   const int K = A.K, G = A.G;
   const Lay L = make_lay(K, G, EXACT, ALGO == 2);
@@ -728,6 +738,23 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   }
   err_dup = __reduce_min_sync(EB_FULL, err_dup);
   if (err_dup != INT_MAX) { put_status(EB_ERR_DUPLICATE_ID, err_dup); return; }
+
+  // The exact integer cost model runs in int64: refuse instances whose
+  // FLOP / byte counts could leave its range (double estimate, 4x margin).
+  {
+    int nmx = 0;
+#pragma unroll
+    for (int h = 0; h < NI; ++h)
+      if (lane + 32 * h < n) nmx = max(nmx, len_i[h]);
+    nmx = __reduce_max_sync(EB_FULL, nmx);
+    const double Ld = (double)C.m.L, dd = (double)C.m.d, fd = (double)C.m.ffn, s = (double)padded, o = (double)nmx;
+    const double bp = (double)C.m.bpp;
+    const double fi = Ld * (8.0 * s * dd * dd + 4.0 * s * s * dd + 4.0 * s * dd * fd);
+    const double far = Ld * o * (8.0 * dd * dd + 4.0 * s * dd + 4.0 * dd * fd + 2.0 * dd * o);
+    const double w = Ld * (4.0 * bp * dd * (double)C.m.head_dim * (double)C.m.heads + 2.0 * bp * dd * fd);
+    const double mem = w + 2.0 * bp * Ld * dd * (s + o) * (double)n;
+    if ((double)n * (fi + far) > 0x1p61 || mem > 0x1p61) { put_status(EB_ERR_OVERFLOW, -1); return; }
+  }
 
   // derive_coefficients feasibility.py:133-167
   const int64_t m1 = weight_bytes(C.m);
@@ -936,6 +963,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   if constexpr (ALGO == 1) { ring_done[lane] = 0; ring_done[lane + 32] = 0; }
   __syncwarp();
 
+  phase_barrier<ALGO>(passed);
   // ---------------- search ------------------------------------------------
   const int total_calls = n * (n + 1) / 2;
   const bool collect = A.prm.collect_trajectory && O.traj && O.traj_offsets;
@@ -946,7 +974,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   int zf = 0, dwin = 0, kwin = 0;
   uint64_t W0 = 0, W1 = 0;
   if constexpr (ALGO == 2) {
-    if (!search_v2<PRUNE, INCL, EXACT, NI>(n, Gi, smem, L, lvl, ncls_d, t_up, t_dn, t_tau, c_len, c_w, o_tau, k2, k3,
+    if (!search_v2<PRUNE, INCL, EXACT, NI>(passed, n, Gi, smem, L, lvl, ncls_d, t_up, t_dn, t_tau, c_len, c_w, o_tau, k2, k3,
                                        slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
                                        tot_v, tot_p)) {
       // leaf counts overflow the u32 unranking tables: hand the instance to
@@ -1037,6 +1065,8 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   }
   }  // v1
 
+  if constexpr (ALGO == 1) phase_barrier<1>(passed);   // (ALGO 2 passed its own)
+  phase_barrier<ALGO>(passed);
   // ---------------- finish ------------------------------------------------
   int status = EB_OK;
   double met[EB_N_METRICS];
@@ -1144,8 +1174,30 @@ __global__ void __launch_bounds__(128, 4) dftsp_kernel(DftspArgs A) {
     inst = __shfl_sync(EB_FULL, inst, 0);
     if (inst >= A.n_inst) break;
     if (A.fallback_pass && A.out.status[inst] != EB_STATUS_FALLBACK) continue;
-    solve_instance<PRUNE, INCL, EXACT, ALGO, NI>(A, inst, smem);
+    int passed = 0;
+    solve_instance<PRUNE, INCL, EXACT, ALGO, NI>(A, inst, smem, passed);
     __syncwarp();
+  }
+}
+
+// Lockstep variant (leaf-parallel algorithm): the block takes one instance
+// per warp per round and all warps cross the same phase barriers.
+template <bool PRUNE, bool INCL, bool EXACT, int NI>
+__global__ void __launch_bounds__(512, 1) dftsp_lock_kernel(DftspArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_all[];
+  __shared__ int s_base;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned char* smem = smem_all + warp * A.warp_bytes;
+  for (;;) {
+    if (threadIdx.x == 0) s_base = atomicAdd(A.counter, nw);
+    __syncthreads();
+    const int64_t base = s_base;
+    if (base >= A.n_inst) break;
+    const int64_t inst = base + warp;
+    int passed = 0;
+    if (inst < A.n_inst) solve_instance<PRUNE, INCL, EXACT, 2, NI>(A, inst, smem, passed);
+    __syncwarp();
+    while (passed < 3) { __syncthreads(); ++passed; }
   }
 }
 
@@ -1259,7 +1311,24 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
     else kern = exact ? dftsp_kernel<false, false, true, AL, NI> : dftsp_kernel<false, false, false, AL, NI>; \
   }
 #define EB_PICK(AL) if (K <= 32) { EB_PICK3(AL, 1) } else { EB_PICK3(AL, 2) }
-  if (algo == 2) { EB_PICK(2) } else { EB_PICK(1) }
+#define EB_PICKL3(NI)                                                                                  \
+  if (P) {                                                                                             \
+    if (I) kern = exact ? dftsp_lock_kernel<true, true, true, NI> : dftsp_lock_kernel<true, true, false, NI>;   \
+    else kern = exact ? dftsp_lock_kernel<true, false, true, NI> : dftsp_lock_kernel<true, false, false, NI>;   \
+  } else {                                                                                             \
+    if (I) kern = exact ? dftsp_lock_kernel<false, true, true, NI> : dftsp_lock_kernel<false, true, false, NI>; \
+    else kern = exact ? dftsp_lock_kernel<false, false, true, NI> : dftsp_lock_kernel<false, false, false, NI>; \
+  }
+  if (algo == 2) {
+    // lockstep blocks: up to 16 warps (one instance each) sharing phases
+    warps = (int)(smem_cap / A.warp_bytes);
+    if (warps > 16) warps = 16;
+    smem = A.warp_bytes * warps;
+    if (K <= 32) { EB_PICKL3(1) } else { EB_PICKL3(2) }
+  } else {
+    EB_PICK(1)
+  }
+#undef EB_PICKL3
   A.fallback_pass = 0;
   EB_CUDA(cudaMemsetAsync(d_counter, 0, 2 * sizeof(int), st));
   int rc = launch_one(h, st, kern, A, warps, smem, n_inst);
