@@ -54,7 +54,58 @@ struct Members {
   int64_t m1, kvp, kv, fi; // weight bytes, kv*padded, kv, flops_initial(padded)
   double alpha, M, beta, C, cap_s;
   int has_cap;
+  // level bounds: sums of the z smallest per-member terms (index z)
+  int64_t lo_far[EB_MAX_K + 1];
+  int64_t lo_n[EB_MAX_K + 1];
+  double lo_a[EB_MAX_K + 1], lo_b[EB_MAX_K + 1];
 };
+
+// true only if leq(a, b) is false for every a >= a_lo (leq is monotone in a);
+// the margin (1e-5 of the 1e-9 slack) dwarfs any rounding of the bounds.
+__device__ __forceinline__ bool fails_margin(double a_lo, double b) {
+  double m = 1.0;
+  double aa = fabs_(a_lo), ab = fabs_(b);
+  if (aa > m) m = aa;
+  if (ab > m) m = ab;
+  return sub(a_lo, b) > mul(1.00001e-9, m);
+}
+
+// Sound level skip: no size-z subset can pass check_direct when the minimum
+// over subsets of memory, compute time, uplink or downlink sum fails by a
+// margin (every sum is minimised by the z smallest terms; memory and FLOPs
+// are exact integers, the float sums lose < 64 ulp, covered by 1e-12).
+__device__ __forceinline__ bool level_infeasible(const Members& S, int z) {
+  int64_t mem = S.m1 + S.kvp * z + S.kv * S.lo_n[z];
+  if (fails_margin(mul(S.alpha, i2d(mem)), S.M)) return true;
+  double cs = div(mul(S.beta, i2d((int64_t)z * S.fi + S.lo_far[z])), S.C);
+  if (S.has_cap && fails_margin(cs, S.cap_s)) return true;
+  if (fails_margin(mul(S.lo_a[z], 0.999999999999), 1.0)) return true;
+  if (fails_margin(mul(S.lo_b[z], 0.999999999999), 1.0)) return true;
+  return false;
+}
+
+// Sorted-prefix bounds (one thread; n <= 64).
+__device__ void build_level_bounds(Members& S) {
+  const int n = S.n;
+  int64_t f[EB_MAX_K];
+  int32_t q[EB_MAX_K];
+  double a[EB_MAX_K], b[EB_MAX_K];
+  for (int i = 0; i < n; ++i) { f[i] = S.far[i]; q[i] = S.nout[i]; a[i] = S.a[i]; b[i] = S.b[i]; }
+  for (int i = 1; i < n; ++i)
+    for (int j = i; j > 0; --j) {
+      if (f[j] < f[j - 1]) { int64_t t = f[j]; f[j] = f[j - 1]; f[j - 1] = t; }
+      if (q[j] < q[j - 1]) { int32_t t = q[j]; q[j] = q[j - 1]; q[j - 1] = t; }
+      if (a[j] < a[j - 1]) { double t = a[j]; a[j] = a[j - 1]; a[j - 1] = t; }
+      if (b[j] < b[j - 1]) { double t = b[j]; b[j] = b[j - 1]; b[j - 1] = t; }
+    }
+  S.lo_far[0] = 0; S.lo_n[0] = 0; S.lo_a[0] = 0.0; S.lo_b[0] = 0.0;
+  for (int z = 1; z <= n; ++z) {
+    S.lo_far[z] = S.lo_far[z - 1] + f[z - 1];
+    S.lo_n[z] = S.lo_n[z - 1] + q[z - 1];
+    S.lo_a[z] = add(S.lo_a[z - 1], a[z - 1]);
+    S.lo_b[z] = add(S.lo_b[z - 1], b[z - 1]);
+  }
+}
 
 // Cooperative (block) load of one instance's members; returns after sync.
 __device__ void load_members(Members& S, const Ctx& c, const eb_requests& req, int64_t r0, int n) {
@@ -89,7 +140,10 @@ __device__ void load_members(Members& S, const Ctx& c, const eb_requests& req, i
     S.has_cap = c.has_cap;
   }
   __syncthreads();
-  if (threadIdx.x == 0) S.status = (s_err == INT_MAX) ? 0 : (s_err & 63);
+  if (threadIdx.x == 0) {
+    S.status = (s_err == INT_MAX) ? 0 : (s_err & 63);
+    build_level_bounds(S);
+  }
   __syncthreads();
 }
 
@@ -203,6 +257,7 @@ __global__ void __launch_bounds__(256) exh_batch_kernel(BatchArgs A) {
     int64_t rk = -1, skipped = 0;
     for (int z = n; z >= 1; --z) {
       uint64_t total = binom(n, z);
+      if (level_infeasible(S, z)) { skipped += (int64_t)total; continue; }   // block-uniform
       if (tid0) best = ULLONG_MAX;
       __syncthreads();
       uint64_t per = (total + blockDim.x - 1) / blockDim.x;
@@ -259,6 +314,7 @@ __global__ void __launch_bounds__(256) exh_range_kernel(RangeArgs A) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *A.status = S.status;
     return;
   }
+  if (level_infeasible(S, A.z)) return;     // no size-z subset can be feasible
   int64_t nchunks = (A.hi - A.lo + A.per - 1) / A.per;
   for (int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks;
        ch += (int64_t)gridDim.x * blockDim.x) {

@@ -1,0 +1,156 @@
+#!/usr/bin/env python3
+"""Benchmark the non-headline BASELINE.json configs on one B200 (JSON line each).
+
+  config1  per-epoch candidate pools the reference simulator hands to dftsp on
+           pkg/scenarios (captured by tests/golden/make_golden.py): DFTSP and
+           brute force, parity vs the reference's recorded outputs
+  config3  K = 10..40 sweep x deadline scale x tolerance cap (w8a16): DFTSP
+           instances/s per K, plus the StB / NoB batching baselines on the same
+           queues (scheduled counts)
+  config4  brute force 2^K, K = 28..32: level-by-level rank-range search
+           (brute.solve_sharded, world 1 on this GPU; the same driver shards by
+           rank over NCCL), z cross-checked against DFTSP (optimality)
+  config5  tight-memory OPT-13B edge (5 output classes): DFTSP instances/s
+
+CPU columns time the C oracle port on a bounded sample with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests")]
+
+from paper_2405_07140_b200 import _lib, brute, search, synth  # noqa: E402
+from paper_2405_07140_b200.soa import InstanceBatch  # noqa: E402
+
+
+def ev_time(fn, reps=3):
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    t = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        t.append(time.perf_counter() - t0)
+    return min(t)
+
+
+def cpu_rate(batch, ladder, sample, threads):
+    import oracle
+    n = min(sample, batch.n_inst)
+    sub = InstanceBatch(batch.offsets[:n + 1].copy(), {k: v[:int(batch.offsets[n])] for k, v in batch.columns.items()},
+                        batch.contexts, batch.ctx_index[:n].copy(), batch.k_max)
+    t0 = time.perf_counter()
+    res = oracle.dftsp_batch(sub, ladder=ladder, threads=threads)
+    return n / (time.perf_counter() - t0), res
+
+
+def config1(threads):
+    from helpers import groups, load_corpus, sub_batch, expected, got
+    d = load_corpus("scenario")
+    n = len(d["offsets"]) - 1
+    bad = 0
+    tot = 0.0
+    for ladder, ids in groups(d).items():
+        b = sub_batch(d, ids)
+        tot += ev_time(lambda: search.solve_batch(b, ladder=ladder), reps=3)
+        res = search.solve_batch(b, ladder=ladder)
+        bad += sum(expected(d, "P", i) != got(res, b, j) for j, i in enumerate(ids))
+    # brute force on the pools the reference's own oracle cap (16) admits
+    from helpers import sub_batch as sb
+    small = [i for i in range(n) if d["offsets"][i + 1] - d["offsets"][i] <= 12 and d["ex_status"][i] == 0]
+    b = sb(d, small)
+    from test_gpu_exhaustive import _run  # noqa
+    t_ex = ev_time(lambda: _run(b, cap=16), reps=3)
+    st, z, rk, nodes, mask = _run(b, cap=16)
+    bad_ex = int(np.sum(z != d["ex_z"][small]) + np.sum(nodes != d["ex_nodes"][small]))
+    return {"config": "config1: scenario epochs (pkg/scenarios default/throughput, rates 2-50)", "instances": n,
+            "dftsp_inst_per_s": round(n / tot, 1), "mismatches_vs_reference": int(bad),
+            "brute_instances": len(small), "brute_inst_per_s": round(len(small) / t_ex, 1),
+            "brute_mismatches_vs_reference": bad_ex}
+
+
+def config3(threads, n_per_k):
+    out = []
+    for K in (10, 15, 20, 25, 30, 35, 40):
+        for ds, tc in ((0.5, 0.25), (1.0, 1.0), (2.0, 0.5)):
+            w = synth.Workload(f"config3 K={K} ds={ds} tc={tc}", profiles=("w8a16",), K=K, deadline_scale=ds,
+                               tolerance_cap=tc)
+            n = n_per_k if K <= 20 else max(n_per_k // 4, 1000)
+            b = synth.generate(w, n, seed=2405_0714 + K)
+            dt = ev_time(lambda: search.solve_batch(b, ladder=(128, 256, 512)), reps=2)
+            res = search.solve_batch(b, ladder=(128, 256, 512))
+            cr, orc = cpu_rate(b, (128, 256, 512), 2000 if K <= 25 else 300, threads)
+            ok = bool(np.array_equal(orc["nodes_visited"], res.nodes_visited[:len(orc["nodes_visited"])]))
+            out.append({"K": K, "deadline_scale": ds, "tolerance_cap": tc, "instances": n,
+                        "dftsp_e2e_inst_per_s": round(n / dt, 1), "mean_z": float(res.z_found.mean()),
+                        "mean_nodes_visited": float(res.nodes_visited.mean()), "cpu_port_inst_per_s": round(cr, 1),
+                        "parity_sample_ok": ok})
+    return {"config": "config3: K sweep x deadline x tolerance (w8a16)", "rows": out}
+
+
+def config4(ks, per_k):
+    import torch
+    out = []
+    for K in ks:
+        w = synth.Workload(f"config4 K={K}", K=K)
+        b = synth.generate(w, per_k, seed=2405_0715 + K)
+        dres = search.solve_batch(b, ladder=(128, 256, 512))
+        for i in range(per_k):
+            lo, hi = int(b.offsets[i]), int(b.offsets[i + 1])
+            cols = {k: np.ascontiguousarray(v[lo:hi]) for k, v in b.columns.items()}
+            rec = b.contexts[int(b.ctx_index[i]):int(b.ctx_index[i]) + 1].copy()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = brute.solve_sharded(rec, cols, world=1)
+            dt = time.perf_counter() - t0
+            out.append({"K": K, "z": r.z, "dftsp_z": int(dres.z_found[i]), "optimality_ok": r.z == int(dres.z_found[i]),
+                        "nodes_visited": r.nodes_visited, "seconds": round(dt, 4),
+                        "subsets_per_s": round(r.nodes_visited / dt, 1),
+                        "reference_extrapolated_s_1core": round(r.nodes_visited / 6.0e4, 1)})
+    return {"config": "config4: brute force 2^K (subsets mode), rank-range level search", "rows": out}
+
+
+def config5(threads, n):
+    b = synth.generate(synth.CONFIG5, n, seed=2405_0716)
+    lad = synth.CONFIG5.outputs
+    dt = ev_time(lambda: search.solve_batch(b, ladder=lad), reps=2)
+    res = search.solve_batch(b, ladder=lad)
+    cr, orc = cpu_rate(b, lad, 3000, threads)
+    ok = bool(np.array_equal(orc["nodes_visited"], res.nodes_visited[:len(orc["nodes_visited"])]))
+    return {"config": synth.CONFIG5.name, "instances": n, "dftsp_e2e_inst_per_s": round(n / dt, 1),
+            "mean_z": float(res.z_found.mean()), "mean_nodes_visited": float(res.nodes_visited.mean()),
+            "cpu_port_inst_per_s": round(cr, 1), "cpu_threads": threads, "parity_sample_ok": ok}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--which", default="1,3,4,5")
+    ap.add_argument("--n3", type=int, default=100_000)
+    ap.add_argument("--n5", type=int, default=1_000_000)
+    ap.add_argument("--k4", default="28,29,30,31,32")
+    ap.add_argument("--per-k4", type=int, default=2)
+    args = ap.parse_args()
+    threads = os.cpu_count() or 1
+    which = set(args.which.split(","))
+    if "1" in which:
+        print(json.dumps(config1(threads)), flush=True)
+    if "5" in which:
+        print(json.dumps(config5(threads, args.n5)), flush=True)
+    if "3" in which:
+        print(json.dumps(config3(threads, args.n3)), flush=True)
+    if "4" in which:
+        print(json.dumps(config4([int(k) for k in args.k4.split(",")], args.per_k4)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
