@@ -115,6 +115,10 @@ typedef struct eb_search_params {
    * its tables fit), 1 = one dfs call per lane (literal node walk),
    * 2 = leaf-parallel enumeration with combinatorial node counts. */
   int32_t algorithm;
+  /* 1 = run exhaustive_optimal(mode="counts") (dftsp.py:316-332) instead of
+   * dftsp: same count-vector sequence, check_knapsack per vector, nodes =
+   * vectors tried (nodes_pruned = 0, counts not reported). */
+  int32_t exhaustive_counts;
 } eb_search_params;
 
 /* Indices into eb_dftsp_result.metrics[i*EB_N_METRICS + m]. */

@@ -58,6 +58,8 @@ def load():
         lib.oracle_work_get.argtypes = [P]
         lib.oracle_exhaustive_level.restype = I64
         lib.oracle_exhaustive_level.argtypes = [P, I32, P, P, P, P, P, P, P, I32, I64, I64]
+        lib.oracle_exhaustive_counts.restype = I32
+        lib.oracle_exhaustive_counts.argtypes = [P, P, I32, P, P, P, P, P, P, P, P, P, P]
         lib.oracle_nob.restype = None
         lib.oracle_nob.argtypes = [P, I32, P, P, P, F64, F64, I32, P, P, P, P]
         _o = lib
@@ -139,3 +141,19 @@ def level_evaluator(ctx_rec, cols):
         return int(r)
 
     return level
+
+
+def exhaustive_counts(ctx_rec, cols, lo, hi, ladder=None):
+    """Oracle exhaustive_optimal(mode='counts') on rows [lo, hi): (status, z, nodes, solution)."""
+    lib = load()
+    n = hi - lo
+    a = {k: np.ascontiguousarray(v[lo:hi]) for k, v in cols.items()}
+    z = C.c_int32(0); nodes = C.c_int64(0)
+    sol = np.full(max(n, 1), -1, np.int32)
+    prm = search_params(ladder=ladder)
+    st = lib.oracle_exhaustive_counts(ctx_rec.ctypes.data, _ref(prm), n, a["id"].ctypes.data,
+                                      a["prompt_tokens"].ctypes.data, a["output_tokens"].ctypes.data,
+                                      a["deadline_s"].ctypes.data, a["waiting_s"].ctypes.data,
+                                      a["channel_gain"].ctypes.data, a["uplink_power_w"].ctypes.data,
+                                      C.byref(z), C.byref(nodes), sol.ctypes.data)
+    return st, z.value, nodes.value, tuple(int(x) for x in sol[:z.value])

@@ -77,7 +77,8 @@ class eb_batch(C.Structure):
 class eb_search_params(C.Structure):
     _fields_ = [("pruning", C.c_int32), ("inclusive_bound", C.c_int32), ("exact_tau", C.c_int32),
                 ("collect_trajectory", C.c_int32), ("ladder_len", C.c_int32),
-                ("ladder", C.c_int32 * EB_MAX_CLASSES), ("algorithm", C.c_int32)]
+                ("ladder", C.c_int32 * EB_MAX_CLASSES), ("algorithm", C.c_int32),
+                ("exhaustive_counts", C.c_int32)]
 
 
 class eb_dftsp_result(C.Structure):

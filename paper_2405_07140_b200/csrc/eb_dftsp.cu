@@ -75,7 +75,7 @@ __host__ __device__ inline Lay make_lay(int K, int G, bool exact, bool v2) {
   if (v2) {
     const int lvls = G > 1 ? G - 1 : 1;
     L.pq = take(4 * (size_t)K * lvls * (K + 2));
-    L.pre = take(4 * 64);
+    L.pre = take(4 * 64 + 8 * 32);
     L.pf = take(16 * (size_t)G * (K + 1));
   } else {
     L.pq = L.pre = L.pf = 0;
@@ -358,17 +358,31 @@ __device__ __forceinline__ void phase_barrier(int& passed) {
   ++passed;
 }
 
+// exhaustive_optimal(mode="counts") (dftsp.py:316-332) rides on the v2 leaf
+// stream: same count vectors in the same order (_count_vectors dftsp.py:335),
+// but the check is check_knapsack's per-member sequential fold over the
+// recovered subset (feasibility.py:170-189) and nodes = vectors tried.
+struct CountsMode {
+  bool on;
+  const int32_t* c_start;   // class member lists (kr order), tau-rank values
+  const uint8_t* c_list;
+  const double* o_key;      // k_up * s  per tau rank
+  const double* o_dnt;      // k_down * n per tau rank
+};
+
 template <bool PRUNE, bool INCL, bool EXACT, int NI>
 __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const Lay& L, const LevelInfo* lvl,
                           const uint8_t* ncls_d, const double* t_up, const double* t_dn, const double* t_tau,
                           const int32_t* c_len, const double* c_w, const double* o_tau, double k2, double k3,
                           double slot_base, bool has_cap, int padded, int64_t* traj, bool& found, int& zf,
                           int& dwin, int& kwin, uint64_t& W0, uint64_t& W1, int& best, uint64_t& tot_v,
-                          uint64_t& tot_p) {
+                          uint64_t& tot_p, const CountsMode& cm) {
   const int lane = threadIdx.x & 31;
+  uint64_t cm_before = 0;   // counts mode: count vectors tried in completed windows
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
   uint32_t* pq = (uint32_t*)(smem + L.pq);
   uint32_t* pre = (uint32_t*)(smem + L.pre);
+  uint64_t* pre64 = (uint64_t*)(smem + L.pre + 4 * 64);
   uint64_t* pfv = (uint64_t*)(smem + L.pf);
   uint64_t* pfp = pfv + (size_t)Gi * (n + 1);
   const int LV = Gi > 1 ? Gi - 1 : 1;
@@ -441,9 +455,11 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       const double lat_cap = EXACT ? slot_cap : pymin(sub(o_tau[d - 1], k3z), slot_cap);
       live = !(fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap));
     }
-    // unranking tables for surviving widths (once per width)
+    // unranking tables for surviving widths (once per width); counts mode
+    // needs every call's vector count, skipped or not
     {
-      const uint64_t bit = live ? (1ULL << (d - 1)) : 0ULL;
+      const bool need = live || (cm.on && c < total_calls);
+      const uint64_t bit = need ? (1ULL << (d - 1)) : 0ULL;
       uint64_t want = (uint64_t)__reduce_or_sync(EB_FULL, (unsigned)bit) |
                       ((uint64_t)__reduce_or_sync(EB_FULL, (unsigned)(bit >> 32)) << 32);
       want &= ~built;
@@ -456,16 +472,28 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       }
       if (!ok) return false;
     }
-    uint32_t cnt = 0;
-    if (live) {
+    uint32_t cnt = 0, nall = 0;
+    if (live || (cm.on && c < total_calls)) {
       const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
       if (ncls_d[d - 1] == 1) {
-        cnt = (z <= row[0].size) ? 1u : 0u;
+        nall = (z <= row[0].size) ? 1u : 0u;
       } else {
         const uint32_t* P1 = pq + (size_t)(d - 1) * LV * W;        // level 1
         const int hi0 = min(z, (int)row[0].size), lo0 = max(0, z - (int)row[0].tail_next);
-        cnt = (hi0 >= lo0) ? P1[z - lo0 + 1] - P1[z - hi0] : 0u;
+        nall = (hi0 >= lo0) ? P1[z - lo0 + 1] - P1[z - hi0] : 0u;
       }
+      cnt = live ? nall : 0u;
+    }
+    uint64_t nall_before = 0, nall_tot = 0;   // counts mode: vectors of earlier calls / whole window
+    if (cm.on) {
+      uint64_t ia = nall;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint64_t t = __shfl_up_sync(EB_FULL, ia, o);
+        if (lane >= o) ia += t;
+      }
+      nall_before = ia - nall;
+      nall_tot = __shfl_sync(EB_FULL, ia, 31);
     }
     uint32_t inc = cnt;
 #pragma unroll
@@ -474,14 +502,16 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       if (lane >= o) inc += t;
     }
     const uint32_t T = __shfl_sync(EB_FULL, inc, 31);
-    if (T == 0) continue;
+    if (T == 0) { cm_before += nall_tot; continue; }
     pre[lane] = inc - cnt;
     pre[32 + lane] = (uint32_t)((z << 8) | d);                      // call of this slot
+    pre64[lane] = nall_before;
     __syncwarp();
     for (uint32_t b0 = 0; b0 < T; b0 += 32) {
       const uint32_t g = b0 + lane;
       bool pass = false;
-      int klast = 0, zz = 0, dd = 0;
+      int klast = 0, zz = 0, dd = 0, slot = 0;
+      uint32_t i0 = 0;
       uint64_t V0 = 0, V1 = 0;
       if (g < T) {
         int a = 0, bnd = 31;                                       // largest slot with pre[slot] <= g
@@ -493,6 +523,8 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
         zz = (int)(zd >> 8);
         dd = (int)(zd & 0xff);
         uint32_t i = g - pre[a];
+        slot = a;
+        i0 = i;
         const double k3z = mul(k3, i2d(zz));
         const double slot_cap = has_cap ? sub(slot_base, k3z) : INF;
         const double mem_cap = sub(k2, i2d((int64_t)padded * zz));
@@ -528,12 +560,41 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
           r -= cc;
         }
         const double cap = EXACT ? pymin(sub(tau, k3z), slot_cap) : pymin(sub(o_tau[dd - 1], k3z), slot_cap);
-        pass = leq(u, 1.0) && leq(dl, 1.0) && leq(i2d(mem), mem_cap) && leq(lat, cap);
+        if (!cm.on) {
+          pass = leq(u, 1.0) && leq(dl, 1.0) && leq(i2d(mem), mem_cap) && leq(lat, cap);
+        } else {
+          // check_knapsack(recover_subset(part, counts), coeff, z, tau_min):
+          // sequential fold over the recovered members (class order, then
+          // cheapest-uplink order among the first dd by tau rank)
+          double up2 = 0.0, dn2 = 0.0, lat2 = 0.0;
+          int64_t mem2 = 0;
+          for (int k = 0; k < m; ++k) {
+            const LevelInfo li = row[k];
+            const int want = getV(V0, V1, k);
+            int taken = 0;
+            for (int p = cm.c_start[li.g]; taken < want; ++p) {
+              const int t = cm.c_list[p];
+              if (t >= dd) continue;
+              up2 = add(up2, cm.o_key[t]);                         // up += k_up * s
+              dn2 = add(dn2, cm.o_dnt[t]);                         // dn += k_down * n
+              mem2 += c_len[li.g];                                 // mem += n
+              lat2 = add(lat2, c_w[li.g]);                         // lat += latency_weight(n)
+              ++taken;
+            }
+          }
+          const double cap2 = pymin(sub(o_tau[dd - 1], k3z), slot_cap);   // min(tau_min, slot_budget(z))
+          pass = leq(up2, 1.0) && leq(dn2, 1.0) && leq(i2d(mem2), mem_cap) && leq(lat2, cap2);
+        }
       }
       const unsigned bal = __ballot_sync(EB_FULL, pass);
       if (bal) {
         const int src = __ffs(bal) - 1;
         found = true;
+        if (cm.on) {
+          const int ws = __shfl_sync(EB_FULL, slot, src);
+          const uint32_t wi = __shfl_sync(EB_FULL, i0, src);
+          tot_v = cm_before + pre64[ws] + wi + 1;
+        }
         zf = __shfl_sync(EB_FULL, zz, src);
         dwin = __shfl_sync(EB_FULL, dd, src);
         kwin = __shfl_sync(EB_FULL, klast, src);
@@ -542,11 +603,17 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
         break;
       }
     }
+    if (!found) cm_before += nall_tot;
     __syncwarp();
   }
   best = found ? (n - zf) * (n - zf + 1) / 2 + (dwin - zf) : INT_MAX;
 
   phase_barrier<2>(passed);
+  if (cm.on) {                       // nodes = count vectors tried; no pruning
+    if (!found) tot_v = cm_before;
+    tot_p = 0;
+    return true;
+  }
   // ---- C: node counts.  Calls (z, d) counted: z > zf (all d >= z), and
   //      z == zf with d < dwin; plus the winner's partial count.
   uint64_t my_v = 0, my_p = 0;
@@ -976,7 +1043,8 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   if constexpr (ALGO == 2) {
     if (!search_v2<PRUNE, INCL, EXACT, NI>(passed, n, Gi, smem, L, lvl, ncls_d, t_up, t_dn, t_tau, c_len, c_w, o_tau, k2, k3,
                                        slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
-                                       tot_v, tot_p)) {
+                                       tot_v, tot_p,
+                                       CountsMode{A.prm.exhaustive_counts != 0, c_start, c_list, o_key, o_dnt})) {
       // leaf counts overflow the u32 unranking tables: hand the instance to
       // the literal walk (second pass of launch_dftsp)
       put_status(EB_STATUS_FALLBACK, -1);
@@ -1293,6 +1361,14 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   // warps per block, 1 = literal lanes-per-call (also v2's in-kernel fallback)
   int algo = prm.algorithm;
   const size_t smem_cap = 227 * 1024;
+  if (prm.exhaustive_counts) {
+    // counts mode exists only in the leaf-parallel search
+    if (prm.exact_tau || al8(make_lay(K, G, exact, true).total) > smem_cap) {
+      set_error("exhaustive counts mode needs the leaf-parallel search (K=%d too large)", K);
+      return EB_ERR_K_TOO_LARGE;
+    }
+    algo = 2;
+  }
   if (algo != 1 && al8(make_lay(K, G, exact, true).total) * 2 > smem_cap) algo = 1;
   if (algo != 1) algo = 2;
   A.warp_bytes = al8(make_lay(K, G, exact, algo == 2).total);

@@ -194,7 +194,8 @@ class BatchResult:
 
 
 def solve_batch(batch: InstanceBatch, *, pruning=True, inclusive_bound=False, exact_tau=False,
-                collect_trajectory=False, ladder=None, device=None, handle=None, algorithm=0) -> BatchResult:
+                collect_trajectory=False, ladder=None, device=None, handle=None, algorithm=0,
+                exhaustive_counts=False) -> BatchResult:
     """K3 over a host InstanceBatch: every instance is one dftsp() call.
 
     ``algorithm``: 0 auto, 1 literal node walk (one dfs call per lane), 2
@@ -220,7 +221,8 @@ def solve_batch(batch: InstanceBatch, *, pruning=True, inclusive_bound=False, ex
         out.traj_offsets = res.traj_offsets.ctypes.data
         out.traj = res.traj.ctypes.data
         out.traj_len = res.traj_len.ctypes.data
-    prm = search_params(pruning, inclusive_bound, exact_tau, collect_trajectory, ladder, algorithm)
+    prm = search_params(pruning, inclusive_bound, exact_tau, collect_trajectory, ladder, algorithm,
+                        exhaustive_counts)
     h = handle or _lib.handle(device)
     b = batch.struct()
     _lib.check(h.lib.eb_dftsp_batch(h.ptr, batch.contexts.ctypes.data, len(batch.contexts), _ref(prm), _ref(b),
@@ -320,6 +322,25 @@ def exhaustive_optimal(candidates, ctx, *, cap: int = 20, mode: str = "subsets",
     return _exhaustive_counts(pool, ctx, ladder)
 
 
+def exhaustive_counts_many(pools, ctx, *, ladder=None, contexts=None, ctx_index=None) -> BatchResult:
+    """exhaustive_optimal(mode="counts") over many pools in one launch (K3 counts mode)."""
+    if contexts is None:
+        contexts = [ctx]
+    recs = np.concatenate([context_record(c) for c in contexts])
+    batch = InstanceBatch.from_pools([list(p) for p in pools], recs, ctx_index)
+    return batch, solve_batch(batch, ladder=ladder, exhaustive_counts=True)
+
+
 def _exhaustive_counts(pool, ctx, ladder) -> SearchOutcome:
-    """Count-vector mode (dftsp.py:316-332): K3 kernel in counts mode."""
-    raise NotImplementedError("exhaustive_optimal(mode='counts') is not implemented on the device yet")
+    """Count-vector mode (dftsp.py:316-332): K3 in counts mode on the device."""
+    batch, res = exhaustive_counts_many([pool], ctx, ladder=ladder)
+    st = int(res.status[0])
+    if st == _lib.ERR_REVERIFY:
+        raise RuntimeError("count-vector solution failed re-verification")
+    raise_for_status(st, pool, int(res.error_index[0]), ctx, ladder)
+    agg = SearchOutcome(nodes_visited=int(res.nodes_visited[0]))
+    z = int(res.z_found[0])
+    if z:
+        agg.solution = [pool[int(j)] for j in res.solution[:z]]
+        agg.z_found = z
+    return agg

@@ -137,9 +137,10 @@ class InstanceBatch:
 
 
 def search_params(pruning=True, inclusive_bound=False, exact_tau=False, collect_trajectory=False, ladder=None,
-                  algorithm=0):
+                  algorithm=0, exhaustive_counts=False):
     p = _lib.eb_search_params()
     p.algorithm = int(algorithm)
+    p.exhaustive_counts = int(bool(exhaustive_counts))
     p.pruning = int(bool(pruning))
     p.inclusive_bound = int(bool(inclusive_bound))
     p.exact_tau = int(bool(exact_tau))

@@ -171,6 +171,31 @@ def run_exhaustive(instances, cap=16):
     return {"ex_status": st, "ex_z": z, "ex_nodes": nodes, "ex_mask": mask}
 
 
+def run_exhaustive_counts(instances, cap=64):
+    """Reference exhaustive_optimal(mode="counts") (dftsp.py:316-332)."""
+    n = len(instances)
+    nreq = sum(len(r) for _, _, r in instances)
+    st = np.zeros(n, np.int32); z = np.zeros(n, np.int32); nodes = np.zeros(n, np.int64)
+    sol = np.full(max(nreq, 1), -1, np.int32)
+    row = 0
+    for i, (ctx, ladder, reqs) in enumerate(instances):
+        try:
+            out = eb.exhaustive_optimal(reqs, ctx, cap=cap, mode="counts", ladder=ladder)
+        except RuntimeError:
+            st[i] = STATUS["reverify"]
+        except ValueError as exc:
+            msg = str(exc)
+            st[i] = STATUS["ladder"] if "ladder" in msg else STATUS["uplink"] if "uplink" in msg else \
+                STATUS["downlink"] if "downlink" in msg else 99
+        else:
+            z[i], nodes[i] = out.z_found, out.nodes_visited
+            if out.solution:
+                idx = {id(r): j for j, r in enumerate(reqs)}
+                sol[row:row + len(out.solution)] = [idx[id(r)] for r in out.solution]
+        row += len(reqs)
+    return {"exc_status": st, "exc_z": z, "exc_nodes": nodes, "exc_solution": sol}
+
+
 def save(name, data, meta):
     path = os.path.join(HERE, f"{name}.npz")
     np.savez_compressed(path, **data)
@@ -181,7 +206,8 @@ def save(name, data, meta):
 
 
 # --------------------------------------------------------------------------
-def corpus_random(seed, count, flagsets=("P", "NP", "PI", "PE", "NL"), exhaustive=True, traj=False, **kw):
+def corpus_random(seed, count, flagsets=("P", "NP", "PI", "PE", "NL"), exhaustive=True, traj=False, counts=False,
+                  **kw):
     rng = np.random.default_rng(seed)
     inst = [random_instance(rng, **kw) for _ in range(count)]
     inst = [(ctx, ladder, reqs) for ladder, ctx, reqs in inst]
@@ -193,6 +219,8 @@ def corpus_random(seed, count, flagsets=("P", "NP", "PI", "PE", "NL"), exhaustiv
             data.update(run_dftsp(inst, tag, FLAGSETS[tag], traj=traj and tag == "P"))
     if exhaustive:
         data.update(run_exhaustive(inst))
+    if counts:
+        data.update(run_exhaustive_counts(inst))
     save(f"random_{seed}", data, {"n_inst": len(inst), "seed": seed, "generator": "conftest.random_instance",
                                   "kwargs": kw, "flagsets": list(flagsets)})
 
@@ -341,14 +369,14 @@ def corpus_units():
 def main():
     quick = "--quick" in sys.argv
     t0 = time.time()
-    corpus_random(2024, 200)
+    corpus_random(2024, 200, counts=True)
     corpus_random(31, 120)
     corpus_random(32, 80, max_requests=12)
     corpus_random(33, 80, max_requests=12)
     corpus_random(34, 20, min_requests=6, max_requests=12, traj=True, flagsets=("P", "NL"))
     corpus_random(35, 100, slot_cap_s=1.0)
     corpus_random(1001, 200)
-    corpus_random(77, 60, max_requests=9)
+    corpus_random(77, 60, max_requests=9, counts=True)
     corpus_units()
     corpus_scenarios(quick)
     corpus_config2(60 if quick else 300)

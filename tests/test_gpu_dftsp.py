@@ -161,3 +161,34 @@ def test_gpu_v2_table_overflow_falls_back_exactly():
     dev = search.solve_batch(batch, ladder=None, algorithm=2)
     orc = oracle.dftsp_batch(batch, ladder=None, threads=4)
     _assert_same(dev, orc, batch, "overflow fallback")
+
+
+@pytest.mark.parametrize("name", ["random_2024", "random_77"])
+def test_gpu_exhaustive_counts_mode_matches_reference(name):
+    d = load_corpus(name)
+    for ladder, ids in groups(d).items():
+        b = sub_batch(d, ids)
+        res = search.solve_batch(b, ladder=ladder, exhaustive_counts=True)
+        for j, i in enumerate(ids):
+            assert int(res.status[j]) == int(d["exc_status"][i]), (i, res.status[j])
+            if res.status[j] == 0:
+                lo = int(b.offsets[j])
+                z = int(res.z_found[j])
+                assert z == int(d["exc_z"][i]) and int(res.nodes_visited[j]) == int(d["exc_nodes"][i]), i
+                lo_d = int(d["offsets"][i])
+                assert tuple(res.solution[lo:lo + z]) == tuple(d["exc_solution"][lo_d:lo_d + z]), i
+
+
+def test_gpu_exhaustive_counts_mode_vs_oracle_fresh():
+    batch, ladders = random_batch(123, 300, k_max=12)
+    for lad, (idx, sb) in group_by_ladder(batch, ladders).items():
+        res = search.solve_batch(sb, ladder=lad, exhaustive_counts=True)
+        for j in range(sb.n_inst):
+            ci = int(sb.ctx_index[j])
+            st, z, nodes, sol = oracle.exhaustive_counts(sb.contexts[ci:ci + 1], sb.columns, int(sb.offsets[j]),
+                                                         int(sb.offsets[j + 1]), ladder=lad)
+            assert int(res.status[j]) == st, j
+            if st == 0:
+                lo = int(sb.offsets[j])
+                assert (int(res.z_found[j]), int(res.nodes_visited[j])) == (z, nodes), j
+                assert tuple(int(x) for x in res.solution[lo:lo + z]) == sol, j
