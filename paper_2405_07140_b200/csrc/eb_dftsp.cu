@@ -618,20 +618,14 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
   //      z == zf with d < dwin; plus the winner's partial count.
   uint64_t my_v = 0, my_p = 0;
   int prev_m = -1;
-  const LevelInfo* prev_row = lvl;
   for (int d = found ? zf : 1; d <= n; ++d) {
     const int m = ncls_d[d - 1];
     const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
     // F(k, .) depends only on levels k..m-1; consecutive widths differ in one
     // class size (and the tails above it), so deeper levels are reused.
     int kc = m - 1;
-    if (m == prev_m) {
-      kc = 0;
-      for (int k = m - 1; k >= 1; --k)
-        if (row[k].size != prev_row[k].size || row[k].tail_next != prev_row[k].tail_next) { kc = k; break; }
-    }
+    if (m == prev_m) kc = row[0].pad[0];     // level of the class that grew (see table build)
     prev_m = m;
-    prev_row = row;
     for (int k = kc; k >= 1; --k) {
       const uint64_t* NV = pfv + (size_t)(k + 1) * (n + 1);
       const uint64_t* NP = pfp + (size_t)(k + 1) * (n + 1);
@@ -1004,6 +998,13 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     ncls_d[d - 1] = (uint8_t)k;
     int tail = 0;
     for (int q = k - 1; q >= 0; --q) { row[q].tail_next = (uint8_t)tail; tail += row[q].size; }
+    // level of the class the d-th request (tau order) joined: the count
+    // recurrence of width d differs from width d-1 only at that level and
+    // above (row[0].pad[0]; meaningful when the class count is unchanged)
+    const int gn = o_g[d - 1];
+    int kn = 0;
+    for (int q = 0; q < k; ++q) if (row[q].g == gn) kn = q;
+    row[0].pad[0] = (uint8_t)kn;
   }
   for (int w = lane; w < nDG; w += 32) {
     int d = w / Gi + 1, g = w % Gi;
@@ -1157,29 +1158,46 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
           if (t < dwin) { sol[q++] = (uint8_t)t; ++taken; }
         }
       }
-      double up = 0.0, dn = 0.0;
-      int64_t sn = 0, fl_pool = 0, fl_batch = 0;
-      int pb = 0;
+    }
+    __syncwarp();
+    // integer sums are order-free: lanes over members, then warp reductions
+    int64_t sn = 0, fl_pool = 0, fl_batch = 0;
+    int pb = 0;
+    for (int j = lane; j < zf; j += 32) {
+      const int t = sol[j];
+      sn += o_len[t];
+      pb = max(pb, o_s[t]);
+      fl_pool += flops_autoregressive(C.m, padded, o_len[t]);
+    }
+    pb = __reduce_max_sync(EB_FULL, pb);
+    for (int j = lane; j < zf; j += 32) fl_batch += flops_autoregressive(C.m, pb, o_len[sol[j]]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sn += __shfl_xor_sync(EB_FULL, sn, o);
+      fl_pool += __shfl_xor_sync(EB_FULL, fl_pool, o);
+      fl_batch += __shfl_xor_sync(EB_FULL, fl_batch, o);
+    }
+    fl_pool += (int64_t)zf * fi_pad;                                   // z * flops_initial + sum(...)
+    const double compute_s = compute_seconds(C, fl_pool);
+    bool late = false;                                                 // per-member deadline checks
+    for (int j = lane; j < zf; j += 32) late |= !leq(add(o_ws[sol[j]], compute_s), o_dl[sol[j]]);
+    late = __any_sync(EB_FULL, late);
+    if (lane == 0) {
+      double up = 0.0, dn = 0.0;                                       // folds in subset order
       for (int j = 0; j < zf; ++j) {
-        int t = sol[j];
+        const int t = sol[j];
         up = add(up, o_key[t]);      // r.prompt_tokens * k_up
         dn = add(dn, o_dnt[t]);      // r.output_tokens * k_down
-        sn += o_len[t];
-        pb = max(pb, o_s[t]);
       }
       int64_t mem = m1 + kv * (int64_t)padded * zf;
       mem += kv * sn;
-      fl_pool = (int64_t)zf * fi_pad;
-      for (int j = 0; j < zf; ++j) fl_pool += flops_autoregressive(C.m, padded, o_len[sol[j]]);
-      double compute_s = compute_seconds(C, fl_pool);
       bool ok = leq(up, 1.0) && leq(dn, 1.0) && leq(mul(C.alpha, i2d(mem)), C.M);
       if (ok && C.has_cap) ok = leq(compute_s, C.cap_s);
-      for (int j = 0; ok && j < zf; ++j) ok = leq(add(o_ws[sol[j]], compute_s), o_dl[sol[j]]);
+      if (ok && late) ok = false;
       if (!ok) status = EB_ERR_REVERIFY;
       // batch_cost at the batch's own padding (sim.py:372-376)
       int64_t mem_b = m1 + kv * (int64_t)pb * zf + kv * sn;
-      fl_batch = (int64_t)zf * flops_initial(C.m, pb);
-      for (int j = 0; j < zf; ++j) fl_batch += flops_autoregressive(C.m, pb, o_len[sol[j]]);
+      fl_batch += (int64_t)zf * flops_initial(C.m, pb);
       met[EB_MET_UP_SUM] = up;
       met[EB_MET_DN_SUM] = dn;
       met[EB_MET_MEM_POOLPAD] = mul(C.alpha, i2d(mem));
