@@ -633,12 +633,36 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       uint64_t* KP = pfp + (size_t)k * (n + 1);
       const LevelInfo li = row[k];
       const bool last = (k == m - 1);
-      warp_prefix2<NI + 1>(n,
-          [&](int r, uint64_t& a, uint64_t& b) {
-            if (r == 0) { a = b = 0; return; }
-            level_counts<PRUNE, INCL>(li, last, r, NV, NP, a, b);
-          },
-          [&](int r, uint64_t a, uint64_t b) { KV[r] = a; KP[r] = b; });
+      if (last) {
+        // deepest level: F(m-1, r) is piecewise constant/linear in r (leaf,
+        // dead end or prune, level_counts), so its prefix sums are closed
+        // forms -- no scan
+        const uint64_t s = li.size;
+        for (int r = lane; r <= n; r += 32) {
+          const uint64_t rr = (uint64_t)r, t = rr < s ? rr : s;
+          uint64_t v, p;
+          if (PRUNE && !INCL) {          // r <= s: (1, r); r > s: (0, s + 1)
+            v = t;
+            p = t * (t + 1) / 2 + (rr - t) * (s + 1);
+          } else if (!PRUNE) {           // r <= s: (1 + r, 0); r > s: (1 + s, 0)
+            v = t + t * (t + 1) / 2 + (rr - t) * (1 + s);
+            p = 0;
+          } else {                       // inclusive: r <= s: 1 + r; s < r <= 2s: 1 + s; r > 2s: prune s + 1
+            const uint64_t u = rr < 2 * s ? rr : 2 * s;
+            v = t + t * (t + 1) / 2 + (u - t) * (1 + s);
+            p = (rr - u) * (s + 1);
+          }
+          KV[r] = v;
+          KP[r] = p;
+        }
+      } else {
+        warp_prefix2<NI + 1>(n,
+            [&](int r, uint64_t& a, uint64_t& b) {
+              if (r == 0) { a = b = 0; return; }
+              level_counts<PRUNE, INCL>(li, false, r, NV, NP, a, b);
+            },
+            [&](int r, uint64_t a, uint64_t b) { KV[r] = a; KP[r] = b; });
+      }
       __syncwarp();
     }
     const LevelInfo l0 = row[0];
