@@ -21,6 +21,7 @@
 //   finish  recover_subset + check_direct re-verification (dftsp.py:276),
 //           solution sorted by id, derived metrics.
 #include <climits>
+#include <cstdlib>
 
 #include "eb_internal.cuh"
 
@@ -1439,8 +1440,11 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   }
   if (algo == 2) {
     // lockstep blocks: up to 16 warps (one instance each) sharing phases
+    // (EB_LOCK_WARPS overrides the width, for tuning)
+    int cap_w = 8;   // measured: 4 -> 44.4, 8 -> 51.6, 12 -> 40.8, 16 -> 50.4 M inst/s (config 2)
+    if (const char* e = getenv("EB_LOCK_WARPS")) { int v = atoi(e); if (v >= 1 && v <= 16) cap_w = v; }
     warps = (int)(smem_cap / A.warp_bytes);
-    if (warps > 16) warps = 16;
+    if (warps > cap_w) warps = cap_w;
     smem = A.warp_bytes * warps;
     if (K <= 32) { EB_PICKL3(1) } else { EB_PICKL3(2) }
   } else {
