@@ -325,9 +325,9 @@ __device__ __forceinline__ void warp_prefix1(int n, ValFn val, StoreFn store) {
 // Full-traversal node counts of one dfs level (dftsp.py:183-234) entered at
 // level k with remaining target r >= 1: (visited, pruned).  PF* = prefix
 // sums over r of F(k+1, .) (index r, F(., 0) = 0).
-template <bool PRUNE, bool INCL>
-__device__ __forceinline__ void level_counts(const LevelInfo& li, bool last, int r, const uint64_t* PFV,
-                                             const uint64_t* PFP, uint64_t& fv, uint64_t& fp) {
+template <bool PRUNE, bool INCL, typename PT>
+__device__ __forceinline__ void level_counts(const LevelInfo& li, bool last, int r, const PT* PFV, const PT* PFP,
+                                             uint64_t& fv, uint64_t& fp) {
   const int s = li.size, cap = li.tail_next + (INCL ? li.size : 0);
   const int x0 = min(r, s);
   const int xs = PRUNE ? max(0, r - cap) : 0;          // lowest unpruned count
@@ -345,8 +345,8 @@ __device__ __forceinline__ void level_counts(const LevelInfo& li, bool last, int
   fp = (PRUNE && xs > 0) ? (uint64_t)xs : 0;            // prune event at x = xs - 1
   const int xb = (x0 == r) ? x0 - 1 : x0;               // descending nodes x = xb .. xs
   if (xb >= xs) {
-    fv += PFV[r - xs] - PFV[r - xb - 1];
-    fp += PFP[r - xs] - PFP[r - xb - 1];
+    fv += (uint64_t)(PFV[r - xs] - PFV[r - xb - 1]);
+    fp += (uint64_t)(PFP[r - xs] - PFP[r - xb - 1]);
   }
 }
 
@@ -370,6 +370,24 @@ struct CountsMode {
   const double* o_key;      // k_up * s  per tau rank
   const double* o_dnt;      // k_down * n per tau rank
 };
+
+// Prefix sums over r of the deepest level's counts (F(m-1, r) is a leaf,
+// dead end or prune; see level_counts), in closed form.
+template <bool PRUNE, bool INCL>
+__device__ __forceinline__ void last_level_prefix(uint64_t s, uint64_t rr, uint64_t& v, uint64_t& p) {
+  const uint64_t t = rr < s ? rr : s;
+  if (PRUNE && !INCL) {            // r <= s: (1, r); r > s: (0, s + 1)
+    v = t;
+    p = t * (t + 1) / 2 + (rr - t) * (s + 1);
+  } else if (!PRUNE) {             // r <= s: (1 + r, 0); r > s: (1 + s, 0)
+    v = t + t * (t + 1) / 2 + (rr - t) * (1 + s);
+    p = 0;
+  } else {                         // inclusive: r <= s: 1 + r; s < r <= 2s: 1 + s; r > 2s: prune s + 1
+    const uint64_t u = rr < 2 * s ? rr : 2 * s;
+    v = t + t * (t + 1) / 2 + (u - t) * (1 + s);
+    p = (rr - u) * (s + 1);
+  }
+}
 
 template <bool PRUNE, bool INCL, bool EXACT, int NI>
 __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const Lay& L, const LevelInfo* lvl,
@@ -617,16 +635,74 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
   }
   // ---- C: node counts.  Calls (z, d) counted: z > zf (all d >= z), and
   //      z == zf with d < dwin; plus the winner's partial count.
+  //      Lanes = pool widths d: each runs the level recurrence for its own
+  //      partition sequentially over r in one u32 row, in place (F(k, r)
+  //      reads PF_{k+1} only at indices <= r, so r descends, then a running
+  //      prefix), inside the prefix-table region that is free once the search
+  //      is done.  The winner's width (it also needs every level for the
+  //      partial count) takes the warp-scan path below.
   uint64_t my_v = 0, my_p = 0;
-  int prev_m = -1;
-  for (int d = found ? zf : 1; d <= n; ++d) {
+  {
+    bool ovf = false;
+    uint32_t* rows = (uint32_t*)(smem + L.t_up);
+    const int W2 = 2 * (n + 1);
+    for (int dbase = found ? zf : 1; dbase <= n; dbase += 32) {
+      const int d = dbase + lane;
+      if (d > n || (found && d == dwin)) continue;
+      const int m = ncls_d[d - 1];
+      const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
+      uint32_t* RV = rows + (size_t)lane * W2;
+      uint32_t* RP = RV + (n + 1);
+      if (m >= 2) {
+        const uint64_t sl = row[m - 1].size;
+        for (int r = 0; r <= d; ++r) {
+          uint64_t v, p;
+          last_level_prefix<PRUNE, INCL>(sl, (uint64_t)r, v, p);
+          ovf |= (v | p) > 0x7fffffffULL;
+          RV[r] = (uint32_t)v;
+          RP[r] = (uint32_t)p;
+        }
+        for (int k = m - 2; k >= 1; --k) {
+          const LevelInfo li = row[k];
+          for (int r = d; r >= 1; --r) {
+            uint64_t fv, fp;
+            level_counts<PRUNE, INCL>(li, false, r, RV, RP, fv, fp);
+            ovf |= (fv | fp) > 0x7fffffffULL;
+            RV[r] = (uint32_t)fv;
+            RP[r] = (uint32_t)fp;
+          }
+          uint64_t av = 0, ap = 0;
+          for (int r = 1; r <= d; ++r) {
+            av += RV[r];
+            ap += RP[r];
+            ovf |= (av | ap) > 0x7fffffffULL;
+            RV[r] = (uint32_t)av;
+            RP[r] = (uint32_t)ap;
+          }
+          RV[0] = RP[0] = 0;
+        }
+      }
+      const LevelInfo l0 = row[0];
+      for (int r = found ? zf : 1; r <= d; ++r) {
+        if (found && r == zf && d > dwin) continue;                // after the winning call
+        uint64_t fv, fp;
+        level_counts<PRUNE, INCL>(l0, m == 1, r, RV, RP, fv, fp);
+        fv += 1;                                                   // the root
+        my_v += fv;
+        my_p += fp;
+        if (traj) {
+          int64_t* tr = traj + 4 * (int64_t)((n - r) * (n - r + 1) / 2 + (d - r));
+          tr[0] = r; tr[1] = d; tr[2] = (int64_t)fv; tr[3] = (int64_t)fp;
+        }
+      }
+    }
+    if (__any_sync(EB_FULL, ovf)) return false;                    // exact literal-walk pass instead
+    __syncwarp();
+  }
+  for (int d = dwin; found && d == dwin; ++d) {
     const int m = ncls_d[d - 1];
     const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
-    // F(k, .) depends only on levels k..m-1; consecutive widths differ in one
-    // class size (and the tails above it), so deeper levels are reused.
-    int kc = m - 1;
-    if (m == prev_m) kc = row[0].pad[0];     // level of the class that grew (see table build)
-    prev_m = m;
+    const int kc = m - 1;    // all levels (the partial count walks them)
     for (int k = kc; k >= 1; --k) {
       const uint64_t* NV = pfv + (size_t)(k + 1) * (n + 1);
       const uint64_t* NP = pfp + (size_t)(k + 1) * (n + 1);
@@ -635,24 +711,9 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       const LevelInfo li = row[k];
       const bool last = (k == m - 1);
       if (last) {
-        // deepest level: F(m-1, r) is piecewise constant/linear in r (leaf,
-        // dead end or prune, level_counts), so its prefix sums are closed
-        // forms -- no scan
-        const uint64_t s = li.size;
         for (int r = lane; r <= n; r += 32) {
-          const uint64_t rr = (uint64_t)r, t = rr < s ? rr : s;
           uint64_t v, p;
-          if (PRUNE && !INCL) {          // r <= s: (1, r); r > s: (0, s + 1)
-            v = t;
-            p = t * (t + 1) / 2 + (rr - t) * (s + 1);
-          } else if (!PRUNE) {           // r <= s: (1 + r, 0); r > s: (1 + s, 0)
-            v = t + t * (t + 1) / 2 + (rr - t) * (1 + s);
-            p = 0;
-          } else {                       // inclusive: r <= s: 1 + r; s < r <= 2s: 1 + s; r > 2s: prune s + 1
-            const uint64_t u = rr < 2 * s ? rr : 2 * s;
-            v = t + t * (t + 1) / 2 + (u - t) * (1 + s);
-            p = (rr - u) * (s + 1);
-          }
+          last_level_prefix<PRUNE, INCL>(li.size, (uint64_t)r, v, p);
           KV[r] = v;
           KP[r] = p;
         }
