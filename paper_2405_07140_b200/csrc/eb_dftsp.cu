@@ -876,12 +876,20 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   __syncwarp();
   // Duplicate ids (coefficients are keyed by id, feasibility.py:164-166).
   int err_dup = INT_MAX;
+  const unsigned active = (n >= 32) ? EB_FULL : ((1u << n) - 1u);
+  if constexpr (NI == 1) {
+    // one request per lane: lanes holding the same id, via a match
+    const unsigned long long key = (lane < n) ? (unsigned long long)id_i[0] : ~0ULL;
+    const unsigned same = __match_any_sync(EB_FULL, key) & active;
+    if (lane < n && (same & lanemask_lt())) err_dup = lane;
+  } else {
 #pragma unroll
-  for (int h = 0; h < NI; ++h) {
-    int i = lane + 32 * h;
-    if (i < n)
-      for (int j = 0; j < i; ++j)
-        if (a_id[j] == id_i[h]) { err_dup = min(err_dup, i); break; }
+    for (int h = 0; h < NI; ++h) {
+      int i = lane + 32 * h;
+      if (i < n)
+        for (int j = 0; j < i; ++j)
+          if (a_id[j] == id_i[h]) { err_dup = min(err_dup, i); break; }
+    }
   }
   err_dup = __reduce_min_sync(EB_FULL, err_dup);
   if (err_dup != INT_MAX) { put_status(EB_ERR_DUPLICATE_ID, err_dup); return; }
@@ -952,6 +960,10 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   // output length with within-class order (key, id) (dftsp.py:71-82).
   int t_i[NI], gcls_i[NI], kr_i[NI];
   bool first_i[NI];
+  unsigned peers = 0;     // NI == 1: lanes with my output length
+  if constexpr (NI == 1) {
+    peers = __match_any_sync(EB_FULL, lane < n ? len_i[0] : -1) & active;
+  }
 #pragma unroll
   for (int h = 0; h < NI; ++h) {
     int i = lane + 32 * h;
@@ -960,10 +972,18 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     if (i < n) {
       int t = 0;
       bool first = true;
-      for (int j = 0; j < n; ++j) {
-        double tj = a_tau[j];
-        t += (tj > tau_i[h]) || (tj == tau_i[h] && a_id[j] < id_i[h]);
-        if (j < i && a_len[j] == len_i[h]) first = false;
+      if constexpr (NI == 1) {
+        for (int j = 0; j < n; ++j) {
+          double tj = a_tau[j];
+          t += (tj > tau_i[h]) || (tj == tau_i[h] && a_id[j] < id_i[h]);
+        }
+        first = (peers & lanemask_lt()) == 0;
+      } else {
+        for (int j = 0; j < n; ++j) {
+          double tj = a_tau[j];
+          t += (tj > tau_i[h]) || (tj == tau_i[h] && a_id[j] < id_i[h]);
+          if (j < i && a_len[j] == len_i[h]) first = false;
+        }
       }
       t_i[h] = t;
       first_i[h] = first;
@@ -1005,12 +1025,22 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     int i = lane + 32 * h;
     if (i < n) {
       int g = 0, kr = 0;
-      for (int j = 0; j < n; ++j) {
-        bool fj = (firstmask >> j) & 1ULL;
-        g += fj && a_len[j] < len_i[h];
-        if (a_len[j] == len_i[h]) {
-          double kj = a_key[j];
+      if constexpr (NI == 1) {
+        // class index: class leaders with a shorter output; rank among peers
+        for (unsigned long long fm = firstmask; fm; fm &= fm - 1) g += a_len[__ffsll((long long)fm) - 1] < len_i[h];
+        for (unsigned pm = peers & ~(1u << lane); pm; pm &= pm - 1) {
+          const int j = __ffs(pm) - 1;
+          const double kj = a_key[j];
           kr += (kj < key_i[h]) || (kj == key_i[h] && a_id[j] < id_i[h]);
+        }
+      } else {
+        for (int j = 0; j < n; ++j) {
+          bool fj = (firstmask >> j) & 1ULL;
+          g += fj && a_len[j] < len_i[h];
+          if (a_len[j] == len_i[h]) {
+            double kj = a_key[j];
+            kr += (kj < key_i[h]) || (kj == key_i[h] && a_id[j] < id_i[h]);
+          }
         }
       }
       gcls_i[h] = g;
