@@ -129,6 +129,14 @@ def max_over_ranks(x: float, world: int, device=None) -> float:
     return float(t.item())
 
 
+def profile_issue_pct():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_dftsp_summary.json")) as fh:
+            return json.load(fh).get("issue_active_pct")
+    except (OSError, ValueError):
+        return None
+
+
 def load_profile_traffic():
     """DRAM bytes per launch of the search kernel from the committed ncu capture (or None)."""
     p = os.path.join(ROOT, "profiles", "ncu_dftsp_summary.json")
@@ -323,7 +331,11 @@ def main():
                      "ops_per_instance": round(ops_per_inst, 1),
                      "ops_model": "26 FP64 ops per leaf check + 5 per descend (SURVEY.md 8(d)); counts from the "
                                   "oracle on a 20k-instance sample of this workload; peak = SMs x 64 FP64 lanes x "
-                                  "max SM clock (no measured FP64 peak in MEASURED_PEAKS.json)"},
+                                  "max SM clock (no measured FP64 peak in MEASURED_PEAKS.json)",
+                     "issue_active_pct_ncu": profile_issue_pct(),
+                     "issue_note": "SM issue-slot utilisation of the search kernel from the committed ncu capture "
+                                   "(profiles/ncu_dftsp_summary.json): the path is instruction-issue bound "
+                                   "(integer control + FP64 compare/accumulate)"},
         "cpu_baseline": {"value": round(cpu_rate, 1), "unit": "instances/s", "cores": threads, "kind": "port",
                          "sample": f"{sub.n_inst} instances of the same workload, C oracle (literal restatement "
                                    f"of the reference), {threads} threads, {cpu_s:.1f} s"},
