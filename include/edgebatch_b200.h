@@ -29,6 +29,7 @@ extern "C" {
 
 #define EB_ABI_VERSION 1
 #define EB_MAX_K 64          /* candidates per instance (u64 subset masks)   */
+#define EB_MAX_K_DFTSP 255   /* dftsp instances: > EB_MAX_K take a wide pass   */
 #define EB_MAX_CLASSES 16    /* output-length classes per instance           */
 #define EB_N_METRICS 8       /* doubles per instance in eb_dftsp_result.metrics */
 
@@ -36,7 +37,7 @@ typedef enum eb_status {
   EB_OK = 0,
   EB_ERR_INVALID_ARG = 1,          /* null pointer, bad size, bad flag               */
   EB_ERR_CUDA = 2,                 /* CUDA runtime failure (eb_last_error())          */
-  EB_ERR_K_TOO_LARGE = 3,          /* instance larger than EB_MAX_K or the call's k_max */
+  EB_ERR_K_TOO_LARGE = 3,          /* instance larger than the entry point's limit or the call's k_max */
   EB_ERR_TOO_MANY_CLASSES = 4,     /* more than EB_MAX_CLASSES distinct output lengths */
   EB_ERR_NO_DEVICE = 5,
   /* Reference exceptions, per instance (status[] value; error_index[] names

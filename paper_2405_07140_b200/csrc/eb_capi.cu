@@ -31,7 +31,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 size_t dftsp_warp_bytes(int K, int G, bool exact);
 int launch_dftsp(eb_handle*, cudaStream_t, const eb_context*, int, const eb_search_params&, int64_t,
                  const int64_t*, const int32_t*, int64_t, const eb_requests&, int, const eb_dftsp_result&,
-                 int64_t, int*);
+                 int64_t, int*, int64_t);
 int launch_dfs_single(eb_handle*, cudaStream_t, int, int, const int32_t*, const int32_t*, const int32_t*,
                       const double*, const double*, const double*, const double*, const double*, int64_t, int,
                       double, const eb_search_params&, int32_t*);
@@ -255,11 +255,11 @@ int32_t eb_dftsp_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, cons
 
   if (mem == EB_MEM_DEVICE) {
     int K = b->k_max;
-    if (K < 1 || K > EB_MAX_K) return EB_ERR_INVALID_ARG;
+    if (K < 1 || K > EB_MAX_K_DFTSP) return EB_ERR_INVALID_ARG;
     int st = ensure_dscratch(h, 256);
     if (st) return st;
     return launch_dftsp(h, h->stream, ctxs, n_ctx, *prm, b->n_inst, b->offsets, b->ctx_index, 0, b->req, K,
-                        *out, 0, (int*)h->dscratch);
+                        *out, 0, (int*)h->dscratch, -1);
   }
   if (mem != EB_MEM_HOST) return EB_ERR_INVALID_ARG;
 
@@ -267,17 +267,21 @@ int32_t eb_dftsp_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, cons
   // (the int64 range of the exact cost model is checked per instance on the
   // device, status EB_ERR_OVERFLOW; only k_max is needed here)
   const int64_t n = b->n_inst;
+  // (the widest instance sizes the kernels; instances wider than EB_MAX_K
+  // take the wide pass, counted here to size its grid)
   int K = b->k_max;
-  if (K <= 0) {
+  int64_t n_wide = 0;
+  if (K <= 0 || K > EB_MAX_K) {      // a k_max <= EB_MAX_K rules out wide instances: skip the scan
     int kk = 0;
     for (int64_t i = 0; i < n; ++i) {
       int64_t sz = b->offsets[i + 1] - b->offsets[i];
       if (sz < 0) return EB_ERR_INVALID_ARG;
-      if (sz > kk) kk = (int)(sz > EB_MAX_K ? EB_MAX_K + 1 : sz);
+      if (sz > kk) kk = (int)(sz > EB_MAX_K_DFTSP ? EB_MAX_K_DFTSP + 1 : sz);
+      n_wide += (sz > EB_MAX_K && sz <= EB_MAX_K_DFTSP);
     }
-    K = kk;
+    if (K <= 0 || kk < K) K = kk;
   }
-  if (K > EB_MAX_K) K = EB_MAX_K;
+  if (K > EB_MAX_K_DFTSP) K = EB_MAX_K_DFTSP;
   if (K < 1) K = 1;
   // Chunking: ~8 chunks for big batches, never below 8192 instances.
   int64_t chunk = (n + 7) / 8;
@@ -323,7 +327,7 @@ int32_t eb_dftsp_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, cons
     }
     int* d_counter = S->alloc<int>(2);
     if (S->err) { rc = S->err; break; }
-    rc = launch_dftsp(h, st, d_ctx[c % 3], n_ctx, *prm, ni, d_off, d_ci, R0, d_req, K, d_out, T0, d_counter);
+    rc = launch_dftsp(h, st, d_ctx[c % 3], n_ctx, *prm, ni, d_off, d_ci, R0, d_req, K, d_out, T0, d_counter, n_wide);
     if (rc) break;
     S->down(out->status + i0, d_out.status, ni);
     S->down(out->error_index ? out->error_index + i0 : nullptr, d_out.error_index, ni);

@@ -847,7 +847,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   int ci = A.ctx_index ? A.ctx_index[inst] : 0;
   if (ci < 0 || ci >= A.n_ctx) { put_status(EB_ERR_INVALID_ARG, -1); return; }
   if (n == 0) { put_status(EB_OK, -1); return; }     // dftsp.py:253-254
-  if (n > K || n > EB_MAX_K) { put_status(EB_ERR_K_TOO_LARGE, -1); return; }
+  if (n > K || n > 32 * NI) { put_status(EB_ERR_K_TOO_LARGE, -1); return; }
   const Ctx C = load_ctx(&A.ctxs[ci]);
 
   // ---------------- setup: per request (lanes over i = lane, lane+32) -----
@@ -990,13 +990,13 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     }
   }
   // class index = number of distinct lengths below mine
-  unsigned long long firstmask = 0;
+  unsigned fmask[NI];     // class leaders: bit (i & 31) of word i >> 5
+  int Gi = 0;
 #pragma unroll
   for (int h = 0; h < NI; ++h) {
-    unsigned b = __ballot_sync(EB_FULL, first_i[h]);
-    firstmask |= (unsigned long long)b << (32 * h);
+    fmask[h] = __ballot_sync(EB_FULL, first_i[h]);
+    Gi += __popc(fmask[h]);
   }
-  const int Gi = __popcll(firstmask);
   if (Gi > G || Gi > EB_MAX_CLASSES) { put_status(EB_ERR_TOO_MANY_CLASSES, -1); return; }
   // Ladder check: the first off-ladder request in tau order (dftsp.py:63-70).
   int bad_t = INT_MAX, bad_i = -1;
@@ -1027,7 +1027,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       int g = 0, kr = 0;
       if constexpr (NI == 1) {
         // class index: class leaders with a shorter output; rank among peers
-        for (unsigned long long fm = firstmask; fm; fm &= fm - 1) g += a_len[__ffsll((long long)fm) - 1] < len_i[h];
+        for (unsigned fm = fmask[0]; fm; fm &= fm - 1) g += a_len[__ffs(fm) - 1] < len_i[h];
         for (unsigned pm = peers & ~(1u << lane); pm; pm &= pm - 1) {
           const int j = __ffs(pm) - 1;
           const double kj = a_key[j];
@@ -1035,7 +1035,10 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
         }
       } else {
         for (int j = 0; j < n; ++j) {
-          bool fj = (firstmask >> j) & 1ULL;
+          unsigned fw = fmask[0];        // fmask[j >> 5] by selects (stays in registers)
+#pragma unroll
+          for (int q = 1; q < NI; ++q) fw = ((j >> 5) == q) ? fmask[q] : fw;
+          bool fj = (fw >> (j & 31)) & 1u;
           g += fj && a_len[j] < len_i[h];
           if (a_len[j] == len_i[h]) {
             double kj = a_key[j];
@@ -1382,6 +1385,29 @@ __global__ void __launch_bounds__(128, 4) dftsp_kernel(DftspArgs A) {
   }
 }
 
+// Wide instances (EB_MAX_K < n <= EB_MAX_K_DFTSP candidates, e.g. a
+// simulator queue with the prefilter off): one warp per block, literal node
+// walk, up to 8 requests per lane; the per-instance tables (O(n^2) prefix
+// sums) live in shared memory when they fit and in a global scratch slab
+// per block otherwise.  Instances come from an atomic counter; the narrow
+// ones were solved by the main pass.
+template <bool PRUNE, bool INCL, bool EXACT>
+__global__ void __launch_bounds__(32, 1) dftsp_wide_kernel(DftspArgs A, unsigned char* gscratch) {
+  extern __shared__ __align__(16) unsigned char smem_all[];
+  unsigned char* smem = gscratch ? gscratch + (size_t)blockIdx.x * A.warp_bytes : smem_all;
+  for (;;) {
+    int64_t inst = 0;
+    if (threadIdx.x == 0) inst = atomicAdd(A.counter, 1);
+    inst = __shfl_sync(EB_FULL, inst, 0);
+    if (inst >= A.n_inst) break;
+    const int64_t n = A.offsets[inst + 1] - A.offsets[inst];
+    if (n <= EB_MAX_K || n > EB_MAX_K_DFTSP) continue;
+    int passed = 0;
+    solve_instance<PRUNE, INCL, EXACT, 1, (EB_MAX_K_DFTSP + 31) / 32>(A, inst, smem, passed);
+    __syncwarp();
+  }
+}
+
 // Lockstep variant (leaf-parallel algorithm): the block takes one instance
 // per warp per round and all warps cross the same phase barriers.
 template <bool PRUNE, bool INCL, bool EXACT, int NI>
@@ -1479,11 +1505,52 @@ static int launch_one(eb_handle* h, cudaStream_t st, void (*kern)(DftspArgs), co
   return EB_OK;
 }
 
+// Second pass over instances wider than EB_MAX_K (see dftsp_wide_kernel).
+static int launch_wide(eb_handle* h, cudaStream_t st, const DftspArgs& A0, int K_all, int64_t n_wide) {
+  DftspArgs W = A0;
+  const int Kw = K_all < EB_MAX_K_DFTSP ? K_all : EB_MAX_K_DFTSP;
+  W.K = Kw;
+  W.G = A0.prm.ladder_len > 0 ? A0.prm.ladder_len : (Kw < EB_MAX_CLASSES ? Kw : EB_MAX_CLASSES);
+  W.fallback_pass = 0;
+  const bool exact = A0.prm.exact_tau != 0;
+  W.warp_bytes = al8(make_lay(Kw, W.G, exact, false).total);
+  const size_t smem_cap = 227 * 1024;
+  const bool in_smem = W.warp_bytes <= smem_cap;
+  int64_t grid = n_wide > 0 ? n_wide : W.n_inst;
+  if (grid > 4 * (int64_t)h->num_sms) grid = 4 * (int64_t)h->num_sms;
+  if (grid < 1) grid = 1;
+  void (*kern)(DftspArgs, unsigned char*);
+  const bool P = W.prm.pruning != 0, I = W.prm.inclusive_bound != 0;
+  if (P) {
+    if (I) kern = exact ? dftsp_wide_kernel<true, true, true> : dftsp_wide_kernel<true, true, false>;
+    else kern = exact ? dftsp_wide_kernel<true, false, true> : dftsp_wide_kernel<true, false, false>;
+  } else {
+    if (I) kern = exact ? dftsp_wide_kernel<false, true, true> : dftsp_wide_kernel<false, true, false>;
+    else kern = exact ? dftsp_wide_kernel<false, false, true> : dftsp_wide_kernel<false, false, false>;
+  }
+  unsigned char* scratch = nullptr;
+  size_t smem = 0;
+  if (in_smem) {
+    smem = W.warp_bytes;
+    EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  } else {
+    EB_CUDA(cudaMallocAsync((void**)&scratch, (size_t)grid * W.warp_bytes, st));
+  }
+  EB_CUDA(cudaMemsetAsync(W.counter, 0, sizeof(int), st));
+  kern<<<(unsigned)grid, 32, smem, st>>>(W, scratch);
+  EB_CUDA(cudaGetLastError());
+  h->launches += 1;
+  if (scratch) EB_CUDA(cudaFreeAsync(scratch, st));
+  return EB_OK;
+}
+
 int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_ctx,
                  const eb_search_params& prm, int64_t n_inst, const int64_t* d_off,
                  const int32_t* d_ctx_index, int64_t req_base, const eb_requests& d_req,
-                 int K, const eb_dftsp_result& d_out, int64_t traj_base, int* d_counter) {
+                 int K, const eb_dftsp_result& d_out, int64_t traj_base, int* d_counter, int64_t n_wide) {
   if (n_inst <= 0) return EB_OK;
+  const int K_all = K;                // widest instance: a wide pass follows when > EB_MAX_K
+  if (K > EB_MAX_K) K = EB_MAX_K;
   int G = prm.ladder_len > 0 ? prm.ladder_len : (K < EB_MAX_CLASSES ? K : EB_MAX_CLASSES);
   if (G < 1) G = 1;
   const bool exact = prm.exact_tau != 0;
@@ -1545,7 +1612,8 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   A.fallback_pass = 0;
   EB_CUDA(cudaMemsetAsync(d_counter, 0, 2 * sizeof(int), st));
   int rc = launch_one(h, st, kern, A, warps, smem, n_inst);
-  if (rc || algo != 2) return rc;
+  if (rc) return rc;
+  if (algo == 2) {
   // literal-walk pass for any instance whose leaf counts overflowed u32
   DftspArgs B = A;
   B.fallback_pass = 1;
@@ -1554,10 +1622,19 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   if (wb > 4) wb = 4;
   EB_PICK(1)
   EB_CUDA(cudaMemsetAsync(d_counter, 0, sizeof(int), st));
-  int rc2 = launch_one(h, st, kern, B, wb, B.warp_bytes * wb, n_inst);
+  rc = launch_one(h, st, kern, B, wb, B.warp_bytes * wb, n_inst);
+  if (rc) return rc;
+  }
 #undef EB_PICK
 #undef EB_PICK3
-  return rc2;
+  if (K_all > EB_MAX_K) {
+    if (prm.exhaustive_counts) {
+      set_error("exhaustive counts mode supports at most %d candidates", EB_MAX_K);
+      return EB_ERR_K_TOO_LARGE;
+    }
+    return launch_wide(h, st, A, K_all, n_wide);
+  }
+  return EB_OK;
 }
 
 int launch_dfs_single(eb_handle* h, cudaStream_t st, int z, int ncls, const int32_t* sizes,

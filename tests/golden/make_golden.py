@@ -315,6 +315,34 @@ def corpus_ksweep(per_k):
     save("ksweep", data, {"n_inst": len(inst), "K": [10, 25, 30, 40]})
 
 
+def _wide_instances():
+    inst = []
+    for K in (65, 96, 128):
+        for ds, tc in ((0.5, 0.25), (1.0, 1.0), (2.0, 0.5)):
+            inst += appendix_d(2405_07150 + K, 2, K, profiles=("w8a16", "fp16"), deadline_scale=ds, tol_cap=tc)
+    inst += appendix_d(2405_07151, 1, 200, profiles=("w8a16",), deadline_scale=0.5, tol_cap=1.0)
+    inst += appendix_d(2405_07152, 1, 255, profiles=("w8a16",), deadline_scale=0.3, tol_cap=1.0)
+    return inst
+
+
+def corpus_wide(parts=("wide", "wide_np")):
+    """Instances wider than EB_MAX_K (64): the device's wide pass, up to EB_MAX_K_DFTSP (255).
+    ``wide``: P/PI/PE on K = 65..255; ``wide_np``: the unpruned search on the K = 65 ones."""
+    inst = _wide_instances()
+    t = time.time()
+    if "wide" in parts:
+        data = pack(inst)
+        for tag in ("P", "PI", "PE"):
+            data.update(run_dftsp(inst, tag, FLAGSETS[tag]))
+        save("wide", data, {"n_inst": len(inst), "K": [65, 96, 128, 200, 255], "generator": "Appendix D, K > 64"})
+    if "wide_np" in parts:
+        small = [x for x in inst if len(x[2]) <= 65]
+        data = pack(small)
+        data.update(run_dftsp(small, "NP", FLAGSETS["NP"]))
+        save("wide_np", data, {"n_inst": len(small), "K": [65], "generator": "Appendix D, K = 65, unpruned"})
+    print(f"    wide corpora: {time.time() - t:.0f} s")
+
+
 def corpus_units():
     """Subset-level goldens: check_direct/check_knapsack/coefficients/batch_cost on random instances."""
     rng = np.random.default_rng(42)
@@ -366,8 +394,47 @@ def corpus_units():
     save("units", data, {"n_inst": len(inst), "n_sub": len(subsets), "seed": 42})
 
 
+SIM_CASES = [
+    ("default.yaml", dict(seed=0, arrival_rate=50.0, duration=12.0)),
+    ("default.yaml", dict(seed=1, arrival_rate=10.0, duration=12.0, compare_pruning=True)),
+    ("throughput.yaml", dict(duration=10.0)),
+    ("default.yaml", dict(seed=2, arrival_rate=30.0, duration=12.0, scheduler="stb", deadline_scale=3.0)),
+    ("default.yaml", dict(seed=3, arrival_rate=30.0, duration=12.0, scheduler="nob", deadline_scale=3.0)),
+    ("default.yaml", dict(seed=4, arrival_rate=5.0, duration=12.0, scheduler="brute")),
+    ("default.yaml", dict(seed=5, arrival_rate=20.0, duration=12.0, verify_oracle=True)),
+    ("default.yaml", dict(seed=6, arrival_rate=40.0, duration=12.0, exact_tau=True, inclusive_prune_bound=True)),
+    ("default.yaml", dict(seed=7, arrival_rate=40.0, duration=12.0, channel_mode="shared")),
+    ("default.yaml", dict(seed=8, arrival_rate=50.0, duration=12.0, quant_profile="w4a16-gptq", tolerance_cap=1.0)),
+    ("default.yaml", dict(seed=9, arrival_rate=30.0, duration=12.0, model="opt-13b", deadline_scale=2.0)),
+    ("default.yaml", dict(seed=10, arrival_rate=60.0, duration=8.0, admission_prefilter=False, accuracy_check=False)),
+]
+
+
+def corpus_sim():
+    """Reference simulator runs (edgebatch.sim.run) for the lock-step batched runner's parity."""
+    from edgebatch import cli, sim
+    out = []
+    for fname, over in SIM_CASES:
+        base = cli.parse_scenario(os.path.join("/root/reference/pkg/scenarios", fname))
+        sc = dataclasses.replace(base, **over)
+        m = sim.run(sc)
+        metrics = {f.name: getattr(m, f.name) for f in dataclasses.fields(m) if f.name != "trace"}
+        trace = [dataclasses.asdict(t) for t in m.trace]
+        scd = dataclasses.asdict(sc)
+        out.append({"scenario": scd, "metrics": metrics, "trace": trace})
+    with open(os.path.join(HERE, "sim_runs.json"), "w") as fh:
+        json.dump(out, fh, indent=0, sort_keys=True)
+    print(f"  sim_runs: {len(out)} runs")
+
+
 def main():
     quick = "--quick" in sys.argv
+    if "--sim-only" in sys.argv:
+        corpus_sim()
+        return
+    if "--wide-only" in sys.argv:
+        corpus_wide(tuple(a for a in sys.argv[2:] if not a.startswith("--")) or ("wide", "wide_np"))
+        return
     t0 = time.time()
     corpus_random(2024, 200, counts=True)
     corpus_random(31, 120)
@@ -382,6 +449,8 @@ def main():
     corpus_config2(60 if quick else 300)
     corpus_config5(20 if quick else 60)
     corpus_ksweep(2 if quick else 4)
+    corpus_wide()
+    corpus_sim()
     print(f"done in {time.time() - t0:.0f} s")
 
 

@@ -25,7 +25,7 @@ FLAGS = {
 }
 RANDOM_CORPORA = ("random_2024", "random_31", "random_32", "random_33", "random_34", "random_35",
                   "random_1001", "random_77")
-ALL_CORPORA = RANDOM_CORPORA + ("scenario", "config2", "config5", "ksweep")
+ALL_CORPORA = RANDOM_CORPORA + ("scenario", "config2", "config5", "ksweep", "wide", "wide_np")
 
 
 def corpus_path(name: str) -> str:

@@ -9,7 +9,7 @@ import pytest
 import oracle
 from gen_random import group_by_ladder, random_batch
 from helpers import ALL_CORPORA, FLAGS, compare_corpus, corpus_path, groups, load_corpus, sub_batch
-from paper_2405_07140_b200 import search
+from paper_2405_07140_b200 import _lib, search
 
 pytestmark = pytest.mark.gpu
 
@@ -192,3 +192,26 @@ def test_gpu_exhaustive_counts_mode_vs_oracle_fresh():
                 lo = int(sb.offsets[j])
                 assert (int(res.z_found[j]), int(res.nodes_visited[j])) == (z, nodes), j
                 assert tuple(int(x) for x in res.solution[lo:lo + z]) == sol, j
+
+
+@pytest.mark.parametrize("tag", ["P", "PE", "PI", "NL"])
+def test_gpu_wide_instances_mixed_with_narrow(tag):
+    """Instances of 1..160 candidates in one call: the narrow ones take the
+    main pass, those over 64 the wide pass; every field equals the oracle."""
+    batch, ladders = random_batch(61, 90, k_min=1, k_max=160, max_classes=3)
+    assert (np.diff(batch.offsets) > 64).sum() >= 20
+    if tag == "NL":
+        parts = {None: (None, batch)}
+    else:
+        parts = group_by_ladder(batch, ladders)
+    for lad, (_, sb) in parts.items():
+        flags = {} if tag == "NL" else FLAGS[tag]
+        dev = search.solve_batch(sb, ladder=lad, **flags)
+        orc = oracle.dftsp_batch(sb, ladder=lad, threads=16, **flags)
+        _assert_same(dev, orc, sb, f"mixed wide/narrow {tag} ladder {lad}")
+
+
+def test_gpu_over_wide_limit_is_k_too_large():
+    batch, _ = random_batch(63, 2, k_min=256, k_max=256, max_classes=3)
+    dev = search.solve_batch(batch, ladder=None)
+    assert (dev.status == _lib.EB_ERR_K_TOO_LARGE).all()

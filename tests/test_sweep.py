@@ -1,0 +1,73 @@
+"""Lock-step batched simulator (paper_2405_07140_b200.sweep) against runs of
+the reference simulator (tests/golden/sim_runs.json, recorded from
+edgebatch.sim.run by tests/golden/make_golden.py --sim-only).  CPU: the
+device entry points are served by the oracle (tests/sweep_oracle.py), which
+checks the simulator's host bookkeeping -- workload draws, expiry, waiting
+times, completions, traces -- independently of the kernels."""
+import json
+import os
+
+import pytest
+
+import sweep_oracle
+from paper_2405_07140_b200 import sweep
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "sim_runs.json")
+
+
+def load_runs():
+    with open(GOLDEN) as fh:
+        return json.load(fh)
+
+
+def compare(got, exp):
+    assert got["error"] is None, got["error"]
+    for k, v in exp["metrics"].items():
+        assert got[k] == v, f"metric {k}: {got[k]} != {v}"
+    assert len(got["trace"]) == len(exp["trace"])
+    for row_g, row_e in zip(got["trace"], exp["trace"]):
+        assert row_g == row_e, f"epoch {row_e['epoch']}: {row_g} != {row_e}"
+
+
+def test_workload_draws_match_reference():
+    for run in load_runs():
+        sc = sweep.Scenario.from_mapping(run["scenario"])
+        import numpy as np
+        w = sweep.generate_workload(sc, np.random.default_rng([sc.seed, 11]))
+        assert len(w) == run["metrics"]["generated"]
+
+
+def test_sweep_host_logic_matches_reference_runs(monkeypatch):
+    sweep_oracle.install(monkeypatch)
+    runs = load_runs()
+    got = sweep.run_many([r["scenario"] for r in runs])
+    for g, e in zip(got, runs):
+        compare(g, e)
+
+
+def test_sweep_runs_are_independent(monkeypatch):
+    """A run's result does not depend on which other runs share its lock-step."""
+    sweep_oracle.install(monkeypatch)
+    runs = load_runs()
+    alone = sweep.run_many([runs[5]["scenario"]])[0]
+    compare(alone, runs[5])
+
+
+def test_sweep_errors_stay_per_run(monkeypatch):
+    sweep_oracle.install(monkeypatch)
+    runs = load_runs()
+    bad = dict(runs[5]["scenario"], oracle_cap=2)            # brute refuses > 2 candidates
+    invalid = dict(runs[0]["scenario"], epoch_s=0.1)         # slots do not fit the epoch
+    got = sweep.run_many([bad, runs[1]["scenario"], invalid])
+    assert got[0]["error"].startswith("ConfigError: scheduler: brute refuses")
+    assert got[2]["error"] == "ConfigError: epoch_s: must fit the uplink and downlink slots"
+    compare(got[1], runs[1])
+
+
+def test_scenario_validation_messages():
+    with pytest.raises(sweep.ConfigError, match="scheduler: must be one of"):
+        sweep.Scenario(scheduler="fifo").validate()
+    with pytest.raises(sweep.ConfigError, match="model/quant_profile"):
+        sweep.Scenario(model="nope").validate()
+    with pytest.raises(sweep.ConfigError, match="deadline_range_s"):
+        sweep.Scenario(deadline_range_s=(2.0, 1.0)).validate()
