@@ -214,4 +214,4 @@ def test_gpu_wide_instances_mixed_with_narrow(tag):
 def test_gpu_over_wide_limit_is_k_too_large():
     batch, _ = random_batch(63, 2, k_min=256, k_max=256, max_classes=3)
     dev = search.solve_batch(batch, ladder=None)
-    assert (dev.status == _lib.EB_ERR_K_TOO_LARGE).all()
+    assert (dev.status == _lib.ERR_K_TOO_LARGE).all()
