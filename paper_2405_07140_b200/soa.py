@@ -82,6 +82,7 @@ def requests_struct(cols: dict) -> eb_requests:
     for name, _ in REQ_FIELDS:
         a = cols.get(name)
         setattr(s, name, ptr(a) if a is not None else None)
+    s._keep = cols          # the struct holds raw pointers: keep the arrays alive with it
     return s
 
 
@@ -117,6 +118,7 @@ class InstanceBatch:
         b.ctx_index = ptr(self.ctx_index)
         b.req = requests_struct(self.columns)
         b.k_max = int(self.k_max)
+        b._keep = self          # raw pointers into this batch's arrays
         return b
 
     def contexts_ptr(self):

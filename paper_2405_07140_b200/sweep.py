@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import time
 from collections import deque
 from dataclasses import dataclass, field, fields
 
@@ -396,7 +397,8 @@ def _costs_and_checks(runs, batches, debug_flags, h):
         spad = pad[chk]
         cst = np.zeros(len(chk), np.int32)
         okc = np.zeros(len(chk), np.uint8)
-        _lib.check(h.lib.eb_check_direct_batch(h.ptr, recs.ctypes.data, n, _ref(requests_struct(request_columns(rows))),
+        cols = request_columns(rows)
+        _lib.check(h.lib.eb_check_direct_batch(h.ptr, recs.ctypes.data, n, _ref(requests_struct(cols)),
                                                len(rows), len(chk), soff.ctypes.data, members.ctypes.data,
                                                sc.ctypes.data, spad.ctypes.data, cst.ctypes.data, okc.ctypes.data,
                                                None, _lib.EB_MEM_HOST), "eb_check_direct_batch")
@@ -409,14 +411,46 @@ def _handle(device):
     return _lib.handle(device)
 
 
-def run_many(scenarios, device=None) -> list:
+_PROFILE: dict | None = None
+
+
+def _tick(name, t0):
+    if _PROFILE is not None:
+        _PROFILE[name] = _PROFILE.get(name, 0.0) + time.perf_counter() - t0
+
+
+def _t(name, fn):
+    """fn, timed into the run_many(profile=...) dict (wall seconds, host packing + device call)."""
+    if _PROFILE is None:
+        return fn
+
+    def timed(*a):
+        t0 = time.perf_counter()
+        try:
+            return fn(*a)
+        finally:
+            _tick(name, t0)
+    return timed
+
+
+def run_many(scenarios, device=None, profile: dict | None = None) -> list:
     """Simulate every scenario in lock-step (each one exactly as sim.run, sim.py:277-412).
 
     Returns one dict per scenario: the SimMetrics fields (sim.py:206-222),
     ``trace`` (EpochTrace rows, sim.py:190-203, as dicts) and ``error``:
     None, or the exception the reference's ``run`` raises for that scenario
     (ConfigError, a search/link ValueError, the compare-pruning or
-    debug-check RuntimeError) -- the other runs continue."""
+    debug-check RuntimeError) -- the other runs continue.  ``profile``: a
+    dict that receives wall seconds per phase."""
+    global _PROFILE
+    _PROFILE = profile
+    try:
+        return _run_many(scenarios, device)
+    finally:
+        _PROFILE = None
+
+
+def _run_many(scenarios, device):
     h = _handle(device)
     runs, failed = [], {}
     for k, sc in enumerate(scenarios):
@@ -432,11 +466,15 @@ def run_many(scenarios, device=None) -> list:
         live = [r for r in live_runs if e <= r.nepochs and r.error is None]
         if not live:
             break
+        t0 = time.perf_counter()
         step = {id(r): _arrivals(r, e) for r in live}
+        _tick("host_arrivals", t0)
         _epoch(live, step, e, h)
+        t0 = time.perf_counter()
         for r in live:
             if r.error is None:
                 _account(r, step[id(r)], e)
+        _tick("host_accounting", t0)
     out = []
     for k, r in enumerate(runs):
         if r is None:
@@ -483,7 +521,7 @@ def _epoch(live, step, e, h):
     for r in by["dftsp"] + by["brute"]:
         groups.setdefault((bool(r.sc.accuracy_check), bool(r.sc.admission_prefilter)), []).append(r)
     for (acc, pre), rs in groups.items():
-        cands = _admission(rs, [r.queue for r in rs], acc, pre, h) if (acc or pre) else [list(r.queue) for r in rs]
+        cands = _t("admission", _admission)(rs, [r.queue for r in rs], acc, pre, h) if (acc or pre) else [list(r.queue) for r in rs]
         for r, c in zip(rs, cands):
             if c is not None:
                 step[id(r)]["cands"] = c
@@ -492,13 +530,13 @@ def _epoch(live, step, e, h):
     for pruning in (True, False):
         grp = [r for r in rs if bool(r.sc.pruning) == pruning]
         if grp:
-            for r, o in zip(grp, _dftsp(grp, [step[id(r)]["cands"] for r in grp], pruning, h)):
+            for r, o in zip(grp, _t("dftsp", _dftsp)(grp, [step[id(r)]["cands"] for r in grp], pruning, h)):
                 if o is not None:
                     step[id(r)]["stats"], step[id(r)]["batch"] = o, o[0]
     rs = ok(rs)
     cmp = [r for r in rs if r.sc.compare_pruning and (e - 1) % r.sc.compare_stride == 0]
     if cmp:
-        for r, o in zip(cmp, _dftsp(cmp, [step[id(r)]["cands"] for r in cmp], False, h)):
+        for r, o in zip(cmp, _t("dftsp_compare", _dftsp)(cmp, [step[id(r)]["cands"] for r in cmp], False, h)):
             if o is None:
                 continue
             st = step[id(r)]
@@ -510,7 +548,7 @@ def _epoch(live, step, e, h):
     orc = [r for r in ok(rs) if r.sc.verify_oracle and (e - 1) % r.oracle_stride == 0
            and len(step[id(r)]["cands"]) <= r.sc.oracle_cap]
     if orc:
-        for r, o in zip(orc, _exhaustive(orc, [step[id(r)]["cands"] for r in orc], h)):
+        for r, o in zip(orc, _t("verify_oracle", _exhaustive)(orc, [step[id(r)]["cands"] for r in orc], h)):
             if o is not None:
                 step[id(r)]["oracle"] = o[1]
 
@@ -522,25 +560,25 @@ def _epoch(live, step, e, h):
         else:
             rs.append(r)
     if rs:
-        for r, o in zip(rs, _exhaustive(rs, [step[id(r)]["cands"] for r in rs], h)):
+        for r, o in zip(rs, _t("brute", _exhaustive)(rs, [step[id(r)]["cands"] for r in rs], h)):
             if o is not None:
                 step[id(r)]["stats"], step[id(r)]["batch"] = o, o[0]
 
     rs = by["stb"]
     if rs:
-        for r, sel in zip(rs, _stb(rs, [r.queue for r in rs], h)):
+        for r, sel in zip(rs, _t("stb", _stb)(rs, [r.queue for r in rs], h)):
             if sel is not None:
                 step[id(r)]["batch"] = sel
     rs = by["nob"]
     if rs:
-        for r, o in zip(rs, _nob(rs, [r.queue for r in rs], [step[id(r)]["t_e"] for r in rs], h)):
+        for r, o in zip(rs, _t("nob", _nob)(rs, [r.queue for r in rs], [step[id(r)]["t_e"] for r in rs], h)):
             if o is not None:
                 st = step[id(r)]
                 st["batch"], st["completions"], st["dropped"] = o
 
     costed = [r for r in ok(live) if step[id(r)]["batch"] and r.sc.scheduler != "nob"]
     if costed:
-        cost, good, status = _costs_and_checks(
+        cost, good, status = _t("cost_check", _costs_and_checks)(
             costed, [step[id(r)]["batch"] for r in costed],
             [r.sc.debug_checks and r.sc.scheduler in ("dftsp", "brute") for r in costed], h)
         for i, r in enumerate(costed):

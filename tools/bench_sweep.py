@@ -53,7 +53,8 @@ def main():
     sweep.run_many(scs[:2])                                    # warm-up: library load, first launches
     l0 = h.launches()
     t = time.perf_counter()
-    out = sweep.run_many(scs)
+    prof = {}
+    out = sweep.run_many(scs, profile=prof)
     dt = time.perf_counter() - t
     errs = sum(o["error"] is not None for o in out)
     epochs = sum(len(o["trace"]) for o in out)
@@ -62,6 +63,7 @@ def main():
                           dftsp_instances=sum(1 for o in out for r in o["trace"]),
                           launches=h.launches() - l0,
                           completed_mean=sum(o.get("completed_total", 0) for o in out) / max(len(out), 1),
+                          phases_s={k: round(v, 3) for k, v in sorted(prof.items())},
                           scenario=scs[0])))
 
 
