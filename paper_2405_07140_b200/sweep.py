@@ -147,17 +147,25 @@ def generate_workload(sc: Scenario, rng) -> list:
         return out
     p_up = dbm_to_watts(sc.uplink_power_dbm)
     lo, hi = sc.deadline_range_s
+    # Same PCG64 draws, cheaper calls: Generator.choice(seq) draws
+    # integers(0, len(seq)), and uniform(lo, hi) is lo + (hi - lo) * random()
+    # (numpy random_uniform); both checked stream-for-stream in tests/test_sweep.py.
+    prompts, outputs = tuple(sc.prompt_choices), tuple(sc.output_classes)
+    npr, nout = len(prompts), len(outputs)
+    span = hi - lo
+    scale = 1.0 / sc.arrival_rate
+    exp, integers, rand = rng.exponential, rng.integers, rng.random
     t = 0.0
     i = 0
     while True:
-        t += rng.exponential(1.0 / sc.arrival_rate)
+        t += exp(scale)
         if t >= sc.duration:
             break
-        prompt = int(rng.choice(sc.prompt_choices))
-        output = int(rng.choice(sc.output_classes))
-        deadline = sc.deadline_scale * float(rng.uniform(lo, hi))
-        tolerance = sc.tolerance_cap * float(rng.uniform(0.0, 1.0))
-        gain = float(rng.exponential(sc.mean_channel_gain))
+        prompt = int(prompts[integers(0, npr)])
+        output = int(outputs[integers(0, nout)])
+        deadline = sc.deadline_scale * float(lo + span * rand())
+        tolerance = sc.tolerance_cap * float(0.0 + (1.0 - 0.0) * rand())
+        gain = float(exp(sc.mean_channel_gain))
         out.append(Request(id=i, prompt_tokens=prompt, output_tokens=output, deadline_s=deadline,
                            tolerance=tolerance, link=UserLink(gain, p_up), arrival_s=t))
         i += 1

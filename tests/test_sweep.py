@@ -37,6 +37,25 @@ def test_workload_draws_match_reference():
         assert len(w) == run["metrics"]["generated"]
 
 
+def test_workload_fast_draws_equal_numpy_calls():
+    """generate_workload's cheaper calls consume the PCG64 stream exactly as
+    the reference's rng.choice / rng.uniform do (sim.py:248-252)."""
+    import numpy as np
+    sc = sweep.Scenario(seed=3, duration=30.0, prompt_choices=(7, 100, 2000, 9), output_classes=(1, 5, 64))
+    fast = sweep.generate_workload(sc, np.random.default_rng([3, 11]))
+    rng = np.random.default_rng([3, 11])
+    t, ref = 0.0, []
+    while True:
+        t += rng.exponential(1.0 / sc.arrival_rate)
+        if t >= sc.duration:
+            break
+        ref.append((t, int(rng.choice(sc.prompt_choices)), int(rng.choice(sc.output_classes)),
+                    sc.deadline_scale * float(rng.uniform(*sc.deadline_range_s)),
+                    sc.tolerance_cap * float(rng.uniform(0.0, 1.0)), float(rng.exponential(sc.mean_channel_gain))))
+    got = [(r.arrival_s, r.prompt_tokens, r.output_tokens, r.deadline_s, r.tolerance, r.link.channel_gain) for r in fast]
+    assert got == ref
+
+
 def test_sweep_host_logic_matches_reference_runs(monkeypatch):
     sweep_oracle.install(monkeypatch)
     runs = load_runs()
