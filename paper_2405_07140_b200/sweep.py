@@ -140,6 +140,55 @@ class Scenario:
         return get_model(self.model, extra_m), get_profile(self.quant_profile, extra_p)
 
 
+@dataclass
+class EpochTrace:
+    """Per-epoch instrumentation row (sim.py:178-195)."""
+
+    epoch: int
+    t_s: float
+    queue_len: int
+    candidates: int
+    batch: int
+    nodes_visited: int
+    nodes_pruned: int
+    nodes_visited_noprune: int | None
+    memory_bytes: float
+    latency_s: float
+    completed: int
+    missed_expired: int
+    missed_late: int
+
+
+@dataclass
+class SimMetrics:
+    """Counters and per-epoch trace of one run (sim.py:197-222), plus the
+    run's failure (``error``/``exception``; None when it completed)."""
+
+    duration_s: float = 0.0
+    epochs: int = 0
+    generated: int = 0
+    scheduled_total: int = 0
+    completed_total: int = 0
+    missed_expired: int = 0
+    missed_late: int = 0
+    dropped_total: int = 0
+    still_queued: int = 0
+    throughput: float = 0.0
+    nodes_visited_total: int = 0
+    nodes_pruned_total: int = 0
+    cmp_nodes_with_pruning: int | None = None
+    cmp_nodes_without_pruning: int | None = None
+    oracle_checks: int = 0
+    oracle_mismatches: int = 0
+    trace: list = field(default_factory=list)
+    error: str | None = field(default=None, compare=False)
+    exception: BaseException | None = field(default=None, compare=False, repr=False)
+
+    @property
+    def missed_total(self) -> int:
+        return self.missed_expired + self.missed_late
+
+
 def generate_workload(sc: Scenario, rng) -> list:
     """Time-ordered request stream, the reference's draw order (sim.py:231-261)."""
     out = []
@@ -190,6 +239,7 @@ class _Run:
     metrics: dict = field(default_factory=dict)
     trace: list = field(default_factory=list)
     error: str | None = None
+    exc: BaseException | None = None
 
 
 def _start(sc: Scenario) -> _Run:
@@ -237,6 +287,7 @@ def _fail(run, exc) -> None:
     """The reference's run() would raise here: the run stops, the others go on."""
     if run.error is None:
         run.error = f"{type(exc).__name__}: {exc}"
+        run.exc = exc
 
 
 def _raise_status(run, status, pool=None, err_index=-1, ladder=None) -> bool:
@@ -466,7 +517,7 @@ def _run_many(scenarios, device):
         try:
             runs.append(_start(sc))
         except ValueError as exc:                     # ConfigError and friends; device errors propagate
-            failed[k] = f"{type(exc).__name__}: {exc}"
+            failed[k] = exc
             runs.append(None)
     live_runs = [r for r in runs if r is not None]
     max_epochs = max((r.nepochs for r in live_runs), default=0)
@@ -486,15 +537,30 @@ def _run_many(scenarios, device):
     out = []
     for k, r in enumerate(runs):
         if r is None:
-            out.append(dict(trace=[], error=failed[k]))
+            exc = failed[k]
+            out.append(SimMetrics(error=f"{type(exc).__name__}: {exc}", exception=exc))
             continue
-        m = dict(r.metrics)
-        m["still_queued"] = len(r.queue) + len(r.pending)
-        m["throughput"] = m["completed_total"] / r.sc.duration
-        m["trace"] = r.trace
-        m["error"] = r.error
+        m = SimMetrics(**r.metrics, trace=[EpochTrace(**row) for row in r.trace], error=r.error, exception=r.exc)
+        m.still_queued = len(r.queue) + len(r.pending)
+        m.throughput = m.completed_total / r.sc.duration
         out.append(m)
     return out
+
+
+def run(sc) -> "SimMetrics":
+    """One scenario, exactly as the reference's ``run`` (sim.py:277-412): its
+    metrics, or the exception it raises."""
+    m = run_many([sc])[0]
+    if m.exception is not None:
+        raise m.exception
+    return m
+
+
+def complexity_reduction(with_pruning, without_pruning):
+    """Node-count reduction in percent; None when no comparison is available (sim.py:224-228)."""
+    if with_pruning is None or without_pruning is None or without_pruning <= 0:
+        return None
+    return 100.0 * (1.0 - with_pruning / without_pruning)
 
 
 def _arrivals(r, e) -> dict:

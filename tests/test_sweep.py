@@ -4,6 +4,7 @@ edgebatch.sim.run by tests/golden/make_golden.py --sim-only).  CPU: the
 device entry points are served by the oracle (tests/sweep_oracle.py), which
 checks the simulator's host bookkeeping -- workload draws, expiry, waiting
 times, completions, traces -- independently of the kernels."""
+import dataclasses
 import json
 import os
 
@@ -21,12 +22,12 @@ def load_runs():
 
 
 def compare(got, exp):
-    assert got["error"] is None, got["error"]
+    assert got.error is None, got.error
     for k, v in exp["metrics"].items():
-        assert got[k] == v, f"metric {k}: {got[k]} != {v}"
-    assert len(got["trace"]) == len(exp["trace"])
-    for row_g, row_e in zip(got["trace"], exp["trace"]):
-        assert row_g == row_e, f"epoch {row_e['epoch']}: {row_g} != {row_e}"
+        assert getattr(got, k) == v, f"metric {k}: {getattr(got, k)} != {v}"
+    assert len(got.trace) == len(exp["trace"])
+    for row_g, row_e in zip(got.trace, exp["trace"]):
+        assert dataclasses.asdict(row_g) == row_e, f"epoch {row_e['epoch']}: {row_g} != {row_e}"
 
 
 def test_workload_draws_match_reference():
@@ -78,8 +79,9 @@ def test_sweep_errors_stay_per_run(monkeypatch):
     bad = dict(runs[5]["scenario"], oracle_cap=2)            # brute refuses > 2 candidates
     invalid = dict(runs[0]["scenario"], epoch_s=0.1)         # slots do not fit the epoch
     got = sweep.run_many([bad, runs[1]["scenario"], invalid])
-    assert got[0]["error"].startswith("ConfigError: scheduler: brute refuses")
-    assert got[2]["error"] == "ConfigError: epoch_s: must fit the uplink and downlink slots"
+    assert got[0].error.startswith("ConfigError: scheduler: brute refuses")
+    assert isinstance(got[0].exception, sweep.ConfigError)
+    assert got[2].error == "ConfigError: epoch_s: must fit the uplink and downlink slots"
     compare(got[1], runs[1])
 
 

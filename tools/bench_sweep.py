@@ -56,13 +56,13 @@ def main():
     prof = {}
     out = sweep.run_many(scs, profile=prof)
     dt = time.perf_counter() - t
-    errs = sum(o["error"] is not None for o in out)
-    epochs = sum(len(o["trace"]) for o in out)
+    errs = sum(o.error is not None for o in out)
+    epochs = sum(len(o.trace) for o in out)
     print(json.dumps(dict(impl="sweep.run_many (lock-step, device)", runs=len(out), errors=errs,
                           seconds=round(dt, 3), runs_per_s=len(out) / dt, epochs=epochs,
-                          dftsp_instances=sum(1 for o in out for r in o["trace"]),
+                          dftsp_instances=epochs,
                           launches=h.launches() - l0,
-                          completed_mean=sum(o.get("completed_total", 0) for o in out) / max(len(out), 1),
+                          completed_mean=sum(o.completed_total for o in out) / max(len(out), 1),
                           phases_s={k: round(v, 3) for k, v in sorted(prof.items())},
                           scenario=scs[0])))
 
