@@ -702,3 +702,159 @@ def _account(r, st, e):
                         batch=len(batch), nodes_visited=nv, nodes_pruned=npr, nodes_visited_noprune=st["trace_np"],
                         memory_bytes=st.get("mem", 0.0), latency_s=st.get("lat", 0.0), completed=completed,
                         missed_expired=st["expired"], missed_late=late))
+
+
+# ---- parameter sweeps and emission (reference cli.py:27-322) -------------
+# The reference's run_sweep runs every (value, seed) point through sim.run,
+# one process per point; here every point is one run of a single lock-step
+# run_many, so each epoch's searches of all points share one launch.
+
+SWEEP_AXES = ("arrival_rate", "deadline_scale", "tolerance_cap", "quant_profile", "model", "scheduler")
+_NUMERIC_AXES = {"arrival_rate", "deadline_scale", "tolerance_cap"}
+COLUMNS = (
+    "kind", "axis", "value", "seed", "scheduler", "model", "quant_profile",
+    "throughput", "completed", "scheduled", "missed", "dropped", "still_queued",
+    "generated", "nodes_visited", "nodes_pruned", "cmp_nodes_with",
+    "cmp_nodes_without", "reduction_pct", "oracle_checks", "oracle_mismatches",
+    "error", "config_hash",
+)
+_AGGREGATE_FIELDS = (
+    "throughput", "completed", "scheduled", "missed", "dropped", "still_queued",
+    "generated", "nodes_visited", "nodes_pruned", "cmp_nodes_with",
+    "cmp_nodes_without", "reduction_pct",
+)
+
+
+@dataclass(frozen=True)
+class SweepSpec:
+    """One swept axis: scenario knob, its values, seeds per value (cli.py:46-60)."""
+
+    axis: str
+    values: tuple
+    repetitions: int = 1
+
+    def __post_init__(self):
+        if self.axis not in SWEEP_AXES:
+            raise ConfigError(f"sweep.axis: must be one of {SWEEP_AXES}")
+        if not self.values:
+            raise ConfigError("sweep.values: must be nonempty")
+        if self.repetitions < 1:
+            raise ConfigError("sweep.repetitions: must be >= 1")
+
+
+def resolved_mapping(sc: Scenario) -> dict:
+    """Every resolved scenario field, tuples as lists (sim.py:166-175)."""
+    out = {}
+    for f in fields(Scenario):
+        v = getattr(sc, f.name)
+        out[f.name] = list(v) if isinstance(v, tuple) else v
+    return out
+
+
+def config_hash(sc: Scenario) -> str:
+    """Stable short hash of the resolved scenario, seed excluded (cli.py:189-194)."""
+    import hashlib
+    import json
+    payload = resolved_mapping(sc)
+    payload.pop("seed", None)
+    blob = json.dumps(payload, sort_keys=True, separators=(",", ":"))
+    return hashlib.sha256(blob.encode()).hexdigest()[:12]
+
+
+def _fmt6(x):
+    if x is None:
+        return None
+    if isinstance(x, (bool, int)):
+        return x
+    return float(f"{float(x):.6g}")
+
+
+def apply_axis(sc: Scenario, axis: str, value) -> Scenario:
+    """Scenario with one sweep axis overridden (cli.py:230-236)."""
+    from dataclasses import replace
+    return replace(sc, **{axis: float(value) if axis in _NUMERIC_AXES else str(value)})
+
+
+def metrics_row(axis, value, sc: Scenario, m: "SimMetrics | None", error: str = "") -> dict:
+    """One data row (cli.py:205-227)."""
+    row = {name: None for name in COLUMNS}
+    row.update(kind="data", axis=axis, value=value, seed=sc.seed, scheduler=sc.scheduler, model=sc.model,
+               quant_profile=sc.quant_profile, error=error, config_hash=config_hash(sc))
+    if m is not None:
+        red = complexity_reduction(m.cmp_nodes_with_pruning, m.cmp_nodes_without_pruning)
+        row.update(throughput=_fmt6(m.throughput), completed=m.completed_total, scheduled=m.scheduled_total,
+                   missed=m.missed_total, dropped=m.dropped_total, still_queued=m.still_queued,
+                   generated=m.generated, nodes_visited=m.nodes_visited_total, nodes_pruned=m.nodes_pruned_total,
+                   cmp_nodes_with=m.cmp_nodes_with_pruning, cmp_nodes_without=m.cmp_nodes_without_pruning,
+                   reduction_pct=_fmt6(red), oracle_checks=m.oracle_checks, oracle_mismatches=m.oracle_mismatches)
+    return row
+
+
+def run_sweep(sc: Scenario, spec: SweepSpec, device=None) -> list:
+    """Every (value, seed) point plus per-value mean/std rows, as cli.run_sweep
+    (cli.py:248-285), with all points simulated in one lock-step run_many."""
+    from dataclasses import replace
+    from statistics import mean, stdev
+    points = []
+    for value in spec.values:
+        varied = apply_axis(sc, spec.axis, value)
+        for rep in range(spec.repetitions):
+            points.append((spec.axis, value, replace(varied, seed=sc.seed + rep)))
+    results = run_many([p[2] for p in points], device=device)
+    rows = []
+    for (axis, value, psc), m in zip(points, results):
+        if m.exception is not None:                  # per-row failure: recorded, sweep continues
+            rows.append(metrics_row(axis, value, psc, None, error=str(m.exception)))
+        else:
+            rows.append(metrics_row(axis, value, psc, m))
+    rows.sort(key=lambda r: (str(r["axis"]), str(r["value"]), r["seed"]))
+    out = []
+    for value in spec.values:
+        group = [r for r in rows if r["value"] == value]
+        out.extend(group)
+        good = [r for r in group if not r["error"]]
+        for kind, fn in (("mean", mean), ("std", lambda v: stdev(v) if len(v) > 1 else 0.0)):
+            agg = {name: None for name in COLUMNS}
+            agg.update(kind=kind, axis=spec.axis, value=value, seed=None,
+                       scheduler=sc.scheduler if spec.axis != "scheduler" else value,
+                       model=sc.model if spec.axis != "model" else value,
+                       quant_profile=sc.quant_profile if spec.axis != "quant_profile" else value,
+                       error="", config_hash=group[0]["config_hash"] if group else "")
+            for name in _AGGREGATE_FIELDS:
+                vals = [r[name] for r in good if r[name] is not None]
+                agg[name] = _fmt6(fn(vals)) if vals else None
+            out.append(agg)
+    return out
+
+
+def _cell(value) -> str:
+    if value is None:
+        return ""
+    if isinstance(value, float):
+        return f"{value:.6g}"
+    return str(value)
+
+
+def emit(table: list, fmt: str, path) -> None:
+    """Result table as CSV or JSON with stable bytes (cli.py:297-312)."""
+    import json
+    from pathlib import Path
+    if not table:
+        raise ValueError("refusing to emit an empty table")
+    if fmt not in ("csv", "json"):
+        raise ValueError(f"unknown format {fmt!r}")
+    path = Path(path)
+    if fmt == "csv":
+        lines = [",".join(COLUMNS)] + [",".join(_cell(row[n]) for n in COLUMNS) for row in table]
+        path.write_text("\n".join(lines) + "\n")
+    else:
+        payload = {"columns": list(COLUMNS), "rows": [{n: row[n] for n in COLUMNS} for row in table]}
+        path.write_text(json.dumps(payload, indent=2, sort_keys=True) + "\n")
+
+
+def emit_trace(m: "SimMetrics", path) -> None:
+    """Per-epoch trace of one run as CSV (cli.py:315-322)."""
+    from pathlib import Path
+    cols = tuple(f.name for f in fields(EpochTrace))
+    lines = [",".join(cols)] + [",".join(_cell(_fmt6(getattr(row, c))) for c in cols) for row in m.trace]
+    Path(path).write_text("\n".join(lines) + "\n")

@@ -427,10 +427,49 @@ def corpus_sim():
     print(f"  sim_runs: {len(out)} runs")
 
 
+SWEEP_CASES = [
+    (dict(duration=8.0, epoch_s=0.5, uplink_slot_s=0.1, downlink_slot_s=0.1), ("arrival_rate", (5, 20, 40), 2)),
+    (dict(duration=8.0, epoch_s=0.5, uplink_slot_s=0.1, downlink_slot_s=0.1, arrival_rate=6.0, seed=3),
+     ("scheduler", ("dftsp", "stb", "nob", "brute"), 2)),
+    (dict(duration=10.0, arrival_rate=20.0, compare_pruning=True, seed=7),
+     ("quant_profile", ("fp16", "w8a16", "w4a16-gptq"), 1)),
+    (dict(duration=10.0, arrival_rate=30.0, seed=11), ("deadline_scale", (0.5, 1.0, 2.0), 2)),
+    (dict(duration=10.0, arrival_rate=15.0, seed=2), ("model", ("bloom-3b", "opt-13b", "nope-1b"), 1)),
+]
+
+
+def corpus_sweeps():
+    """Reference cli.run_sweep tables + emitted bytes, for sweep.run_sweep / emit parity."""
+    import dataclasses
+    import tempfile
+    from edgebatch import cli, sim
+    out = []
+    for over, (axis, values, reps) in SWEEP_CASES:
+        sc = dataclasses.replace(sim.Scenario(), **over)
+        table = cli.run_sweep(sc, cli.SweepSpec(axis, tuple(values), reps))
+        with tempfile.TemporaryDirectory() as d:
+            cli.emit(table, "csv", f"{d}/t.csv")
+            cli.emit(table, "json", f"{d}/t.json")
+            csv_text = open(f"{d}/t.csv").read()
+            json_text = open(f"{d}/t.json").read()
+        out.append({"scenario": sim.resolved_mapping(sc), "axis": axis, "values": list(values), "repetitions": reps,
+                    "rows": table, "csv": csv_text, "json": json_text})
+    sc = dataclasses.replace(sim.Scenario(), duration=8.0, arrival_rate=25.0, compare_pruning=True, seed=4)
+    m = sim.run(sc)
+    with tempfile.TemporaryDirectory() as d:
+        cli.emit_trace(m, f"{d}/trace.csv")
+        trace_text = open(f"{d}/trace.csv").read()
+    with open(os.path.join(HERE, "sim_sweeps.json"), "w") as fh:
+        json.dump({"sweeps": out, "trace_run": {"scenario": sim.resolved_mapping(sc), "csv": trace_text}}, fh,
+                  indent=0, sort_keys=True)
+    print(f"  sim_sweeps: {len(out)} sweeps")
+
+
 def main():
     quick = "--quick" in sys.argv
     if "--sim-only" in sys.argv:
         corpus_sim()
+        corpus_sweeps()
         return
     if "--wide-only" in sys.argv:
         corpus_wide(tuple(a for a in sys.argv[2:] if not a.startswith("--")) or ("wide", "wide_np"))
@@ -451,6 +490,7 @@ def main():
     corpus_ksweep(2 if quick else 4)
     corpus_wide()
     corpus_sim()
+    corpus_sweeps()
     print(f"done in {time.time() - t0:.0f} s")
 
 

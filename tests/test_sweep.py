@@ -92,3 +92,43 @@ def test_scenario_validation_messages():
         sweep.Scenario(model="nope").validate()
     with pytest.raises(sweep.ConfigError, match="deadline_range_s"):
         sweep.Scenario(deadline_range_s=(2.0, 1.0)).validate()
+
+
+SWEEPS = os.path.join(os.path.dirname(__file__), "golden", "sim_sweeps.json")
+
+
+def load_sweeps():
+    with open(SWEEPS) as fh:
+        return json.load(fh)
+
+
+def check_sweeps(tmp_path):
+    """sweep.run_sweep + emit against the reference's cli.run_sweep tables and bytes."""
+    d = load_sweeps()
+    for k, case in enumerate(d["sweeps"]):
+        sc = sweep.Scenario.from_mapping(case["scenario"])
+        table = sweep.run_sweep(sc, sweep.SweepSpec(case["axis"], tuple(case["values"]), case["repetitions"]))
+        assert len(table) == len(case["rows"])
+        for got, exp in zip(table, case["rows"]):
+            assert got == exp, f"sweep {k}: {got} != {exp}"
+        sweep.emit(table, "csv", tmp_path / f"{k}.csv")
+        sweep.emit(table, "json", tmp_path / f"{k}.json")
+        assert (tmp_path / f"{k}.csv").read_text() == case["csv"]
+        assert (tmp_path / f"{k}.json").read_text() == case["json"]
+    tr = d["trace_run"]
+    m = sweep.run(sweep.Scenario.from_mapping(tr["scenario"]))
+    sweep.emit_trace(m, tmp_path / "trace.csv")
+    assert (tmp_path / "trace.csv").read_text() == tr["csv"]
+
+
+def test_sweep_tables_and_emission_match_reference(monkeypatch, tmp_path):
+    sweep_oracle.install(monkeypatch)
+    check_sweeps(tmp_path)
+
+
+def test_config_hash_matches_reference():
+    for case in load_sweeps()["sweeps"]:
+        sc = sweep.Scenario.from_mapping(case["scenario"])
+        data_rows = [r for r in case["rows"] if r["kind"] == "data"]
+        assert any(sweep.config_hash(sweep.apply_axis(sc, case["axis"], r["value"])) == r["config_hash"]
+                   for r in data_rows)
