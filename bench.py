@@ -46,7 +46,7 @@ LADDER = (128, 256, 512)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--n-inst", type=int, default=1_000_000, help="instances per GPU")
@@ -56,20 +56,53 @@ def parse():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region (NVML
+    every 2 ms from a thread; nvidia-smi -lms as the fallback)."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []
+        self.rows = []          # (sm_mhz, max_mhz, reasons bitmask)
         self.proc = None
+        self.stop = threading.Event()
+        self.thread = None
 
     def __enter__(self):
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            idx = self.device
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                try:
+                    idx = int(vis.split(",")[self.device])
+                except ValueError:
+                    pass
+            hnd = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(hnd, pynvml.NVML_CLOCK_SM)
+
+            def loop():
+                while not self.stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(hnd)
+                        self.rows.append((float(sm), float(mx), int(rs)))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            pass
+        try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,"
-                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -78,27 +111,31 @@ class ClockSampler:
         return self
 
     def _read(self):
+        bits = (0x8, 0x40, 0x20, 0x4)
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.rows.append(parts)
+            try:
+                mask = sum(b for b, v in zip(bits, parts[2:6]) if v.lower() == "active")
+                self.rows.append((float(parts[0]), float(parts[1]), mask))
+            except (ValueError, IndexError):
+                pass
 
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=5)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[j] for r in self.rows for j in range(4) if r[3 + j].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+        reasons = sorted({name for _, _, m in self.rows for bit, name in self.REASONS.items() if m & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
                 "reasons": reasons, "samples": len(self.rows)}
 
 
@@ -252,9 +289,11 @@ def main():
     # ---- e2e through the C ABI with pinned host buffers --------------------
     e2e = None
     if not args.no_e2e:
-        pin = {k: torch.from_numpy(np.ascontiguousarray(batch.columns[k])).pin_memory() for k in used}
-        p_off = torch.from_numpy(batch.offsets).pin_memory()
-        p_ci = torch.from_numpy(batch.ctx_index).pin_memory()
+        from paper_2405_07140_b200.soa import pack_wire
+
+        def pinned(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
         hout = {"status": torch.zeros(n, dtype=torch.int32).pin_memory(),
                 "z_found": torch.zeros(n, dtype=torch.int32).pin_memory(),
                 "nodes_visited": torch.zeros(n, dtype=torch.int64).pin_memory(),
@@ -263,34 +302,51 @@ def main():
         hres = _lib.eb_dftsp_result()
         for k, t in hout.items():
             setattr(hres, k, t.data_ptr())
-        hb = InstanceBatch(p_off, pin, batch.contexts, p_ci, batch.k_max).struct()
-        h2d = sum(t.numel() * t.element_size() for t in pin.values()) + p_off.numel() * 8 + p_ci.numel() * 4
         d2h = sum(t.numel() * t.element_size() for t in hout.values())
+        # wide layout (eb_requests, 48 B/request) and the compact wire format
+        # (eb_requests_packed, 32 B/request); the same pinned output buffers
+        hb = InstanceBatch(pinned(batch.offsets), {k: pinned(batch.columns[k]) for k in used}, batch.contexts,
+                           pinned(batch.ctx_index), batch.k_max)
+        h2d_wide = sum(hb.columns[k].nbytes for k in used) + hb.offsets.nbytes + hb.ctx_index.nbytes
+        wb = pack_wire(batch, pin=pinned)
+        assert wb is not None, "config-2 columns narrow losslessly"
+        hbs, wbs = hb.struct(), wb.struct()
 
-        def step_host():
+        def step_wide():
             _lib.check(h.lib.eb_dftsp_batch(h.ptr, batch.contexts.ctypes.data, len(batch.contexts), ref(prm),
-                                            ref(hb), ref(hres), _lib.EB_MEM_HOST), "eb_dftsp_batch(host)")
+                                            ref(hbs), ref(hres), _lib.EB_MEM_HOST), "eb_dftsp_batch(host)")
 
-        for _ in range(max(1, args.warmup)):
-            step_host()
-        barrier(world)
-        torch.cuda.synchronize()
-        et = []
-        for _ in range(args.steps):
-            flush.fill_(1.0)
+        def step_wire():
+            _lib.check(h.lib.eb_dftsp_batch_packed(h.ptr, batch.contexts.ctypes.data, len(batch.contexts), ref(prm),
+                                                   ref(wbs), ref(hres), _lib.EB_MEM_HOST), "eb_dftsp_batch_packed")
+
+        def time_host(step):
+            for _ in range(max(1, args.warmup)):
+                step()
+            barrier(world)
             torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            step_host()
-            e1.record(stream)
-            e1.synchronize()
-            et.append(e0.elapsed_time(e1) / 1e3)
-        e2e_s = max_over_ranks(sum(et), world, dev)
-        assert np.array_equal(hout["z_found"].numpy(), z)
-        e2e = {"value": world * n * args.steps / e2e_s, "unit": "instances/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s / args.steps * 1e3,
-               "path": "eb_dftsp_batch(EB_MEM_HOST), pinned host buffers, 3-stream chunk pipeline"}
+            et = []
+            for _ in range(args.steps):
+                flush.fill_(1.0)
+                torch.cuda.synchronize()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                step()
+                e1.record(stream)
+                e1.synchronize()
+                et.append(e0.elapsed_time(e1) / 1e3)
+            assert np.array_equal(hout["z_found"].numpy(), z) and np.array_equal(hout["nodes_visited"].numpy(), vis)
+            return max_over_ranks(sum(et), world, dev)
+
+        wide_s = time_host(step_wide)
+        wire_s = time_host(step_wire)
+        e2e = {"value": world * n * args.steps / wire_s, "unit": "instances/s", "h2d_bytes_per_step": int(wb.nbytes()),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": wire_s / args.steps * 1e3,
+               "path": "eb_dftsp_batch_packed(EB_MEM_HOST): pinned host buffers in the compact wire format "
+                       "(id i32, tokens u16, uniform uplink power), 16-chunk 3-stream pipeline",
+               "wide": {"value": world * n * args.steps / wide_s, "h2d_bytes_per_step": int(h2d_wide),
+                        "ms_per_step": wide_s / args.steps * 1e3, "path": "eb_dftsp_batch(EB_MEM_HOST), eb_requests"}}
 
     # ---- roofline (rank 0 figures) + cpu baseline ---------------------------
     import oracle

@@ -181,6 +181,45 @@ int32_t eb_dftsp_batch(eb_handle *h, const eb_context *ctxs, int32_t n_ctx,
                        const eb_search_params *params, const eb_batch *batch,
                        eb_dftsp_result *out, int32_t mem);
 
+/* ---- K3 over the compact wire format ------------------------------------
+ * Same search and results as eb_dftsp_batch (dftsp.py:237-285), for host
+ * callers whose request columns fit narrower types.  Fewer bytes cross
+ * PCIe per request: 4 (id) + 2 + 2 (tokens) + 3 x 8 (deadline, waiting,
+ * gain), plus 8 for uplink power unless it is uniform.  That is 32 B instead
+ * of eb_requests' 48 B.  Each chunk is copied in this layout and widened on
+ * the device by a copy kernel into eb_requests columns, so the search
+ * reads exactly the values the wide call would.  Every narrowing is
+ * lossless: Request.id (feasibility.py:35) and the token counts
+ * (feasibility.py:36-37) are Python ints.  The caller checks they fit
+ * (paper_2405_07140_b200/soa.py pack_wire does). */
+typedef struct eb_requests_packed {
+  const int32_t *id;
+  const uint16_t *prompt_tokens;
+  const uint16_t *output_tokens;
+  const double *deadline_s;
+  const double *waiting_s;
+  const double *channel_gain;
+  const double *uplink_power_w;   /* n_req values, or 1 if uplink_power_uniform */
+  int32_t uplink_power_uniform;   /* 1: every request has uplink_power_w[0]     */
+  int32_t _pad;
+} eb_requests_packed;
+
+typedef struct eb_batch_packed {
+  int64_t n_inst;
+  int64_t n_req;              /* == offsets[n_inst] */
+  const int64_t *offsets;     /* n_inst + 1 */
+  const int32_t *ctx_index;   /* n_inst, or NULL = context 0 for all */
+  eb_requests_packed req;
+  int32_t k_max;              /* required: max offsets[i+1]-offsets[i] (<= EB_MAX_K) */
+  int32_t _pad;
+} eb_batch_packed;
+
+/* Host memory only (mem must be EB_MEM_HOST): the wire format exists to cut
+ * host->device bytes.  Device-resident callers use eb_dftsp_batch. */
+int32_t eb_dftsp_batch_packed(eb_handle *h, const eb_context *ctxs, int32_t n_ctx,
+                              const eb_search_params *params, const eb_batch_packed *batch,
+                              eb_dftsp_result *out, int32_t mem);
+
 /* ---- K3': one dfs() call on a prepared partition ----------------------
  * Replaces dfs(z, part, coeff, tau_min, ...) dftsp.py:135-234.  The
  * partition (ClassPartition dftsp.py:29-39) is given class-major: n_cls

@@ -44,15 +44,31 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
         os.path.join(ROOT, "include", "edgebatch_b200.h")]
     if not force and not _stale(LIB, deps):
         return LIB
-    cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-shared",
-           "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *srcs]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
+             "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v" if verbose else "-O3",
+             "-I", os.path.join(ROOT, "include")]
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        return obj, subprocess.run([_nvcc(), *flags, "-c", "-o", obj, src], capture_output=True, text=True)
+
+    # one nvcc per translation unit, in parallel (eb_dftsp.cu dominates)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    for _, res in results:
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed building libedgebatch_b200.so")
+        if verbose:
+            sys.stderr.write(res.stderr)
+    res = subprocess.run([_nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *[o for o, _ in results]],
+                         capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libedgebatch_b200.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libedgebatch_b200.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

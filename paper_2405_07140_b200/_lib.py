@@ -74,6 +74,17 @@ class eb_batch(C.Structure):
                 ("req", eb_requests), ("k_max", C.c_int32), ("_pad", C.c_int32)]
 
 
+class eb_requests_packed(C.Structure):
+    _fields_ = [("id", C.c_void_p), ("prompt_tokens", C.c_void_p), ("output_tokens", C.c_void_p),
+                ("deadline_s", C.c_void_p), ("waiting_s", C.c_void_p), ("channel_gain", C.c_void_p),
+                ("uplink_power_w", C.c_void_p), ("uplink_power_uniform", C.c_int32), ("_pad", C.c_int32)]
+
+
+class eb_batch_packed(C.Structure):
+    _fields_ = [("n_inst", C.c_int64), ("n_req", C.c_int64), ("offsets", C.c_void_p), ("ctx_index", C.c_void_p),
+                ("req", eb_requests_packed), ("k_max", C.c_int32), ("_pad", C.c_int32)]
+
+
 class eb_search_params(C.Structure):
     _fields_ = [("pruning", C.c_int32), ("inclusive_bound", C.c_int32), ("exact_tau", C.c_int32),
                 ("collect_trajectory", C.c_int32), ("ladder_len", C.c_int32),
@@ -101,6 +112,7 @@ _SIGS = {
     "eb_synchronize": (I32, [P]),
     "eb_kernel_launches": (I64, [P]),
     "eb_dftsp_batch": (I32, [P, P, I32, P, P, P, I32]),
+    "eb_dftsp_batch_packed": (I32, [P, P, I32, P, P, P, I32]),
     "eb_dfs_single": (I32, [P, I32, I32, P, P, P, P, P, P, P, P, I64, I32, F64, P, P, P, P, P]),
     "eb_exhaustive_batch": (I32, [P, P, I32, P, I32, P, P, P, P, P, I32]),
     "eb_exhaustive_level_range": (I32, [P, P, I32, P, I32, I64, I64, P]),

@@ -139,10 +139,142 @@ eb_requests upload_req(Stage& S, const eb_requests& r, int64_t lo, int64_t n) {
   return d;
 }
 
+// Wire format -> eb_requests columns (lossless widening; uniform uplink
+// power broadcast).  deadline/waiting/gain are already f64 and stay in place.
+__global__ void widen_wire_kernel(int64_t nr, const int32_t* __restrict__ id32,
+                                  const uint16_t* __restrict__ p16, const uint16_t* __restrict__ o16,
+                                  const double* __restrict__ pw, int uniform, int64_t* __restrict__ id64,
+                                  int32_t* __restrict__ p32, int32_t* __restrict__ o32, double* __restrict__ pw64) {
+  const double pw0 = uniform ? pw[0] : 0.0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nr; j += (int64_t)gridDim.x * blockDim.x) {
+    id64[j] = id32[j];
+    p32[j] = p16[j];
+    o32[j] = o16[j];
+    pw64[j] = uniform ? pw0 : pw[j];
+  }
+}
+
+eb_requests upload_wire(Stage& S, const eb_requests_packed& r, int64_t lo, int64_t n) {
+  eb_requests d;
+  memset(&d, 0, sizeof(d));
+  const int32_t* id32 = S.up(r.id + lo, n);
+  const uint16_t* p16 = S.up(r.prompt_tokens + lo, n);
+  const uint16_t* o16 = S.up(r.output_tokens + lo, n);
+  d.deadline_s = S.up(r.deadline_s + lo, n);
+  d.waiting_s = S.up(r.waiting_s + lo, n);
+  d.channel_gain = S.up(r.channel_gain + lo, n);
+  const double* pw = r.uplink_power_uniform ? S.up(r.uplink_power_w, 1) : S.up(r.uplink_power_w + lo, n);
+  int64_t* id64 = S.alloc<int64_t>(n);
+  int32_t* p32 = S.alloc<int32_t>(n);
+  int32_t* o32 = S.alloc<int32_t>(n);
+  double* pw64 = S.alloc<double>(n);
+  if (S.err) return d;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 8 * S.h->num_sms) blocks = 8 * S.h->num_sms;
+  if (blocks < 1) blocks = 1;
+  widen_wire_kernel<<<blocks, 256, 0, S.st>>>(n, id32, p16, o16, pw, r.uplink_power_uniform != 0, id64, p32,
+                                               o32, pw64);
+  ++S.h->launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { S.err = cuda_fail(e, "widen_wire_kernel"); return d; }
+  d.id = id64;
+  d.prompt_tokens = p32;
+  d.output_tokens = o32;
+  d.uplink_power_w = pw64;
+  return d;
+}
+
 bool req_complete(const eb_requests& r, bool need_tol) {
   return r.id && r.prompt_tokens && r.output_tokens && r.deadline_s && r.waiting_s && r.channel_gain &&
          r.uplink_power_w && (!need_tol || r.tolerance);
 }
+
+// Host-memory DFTSP: instance chunks pipelined over the handle's three
+// staging streams (H2D of chunk c+1 overlaps the search of chunk c and the
+// D2H of chunk c-1).  `upload(S, R0, nr)` stages request rows [R0, R0+nr)
+// and returns their device columns (wide or wire format).
+template <typename Upload>
+int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const eb_search_params& prm, int64_t n,
+                        const int64_t* offsets, const int32_t* ctx_index, int K, int64_t n_wide,
+                        const eb_dftsp_result& out, Upload upload) {
+  // Chunking: ~16 chunks for big batches (the first chunk's copy and the
+  // last chunk's search are the exposed pipeline fill), never below 8192
+  // instances.
+  int64_t chunk = (n + 15) / 16;
+  if (chunk < 8192) chunk = 8192;
+  const int nchunks = (int)((n + chunk - 1) / chunk);
+  // The pipeline streams fork from / join back into the handle's stream so
+  // events a caller records on that stream bracket the whole host->host call.
+  EB_CUDA(cudaEventRecord(h->ev[0], h->stream));
+  for (int i = 0; i < 3; ++i) EB_CUDA(cudaStreamWaitEvent(h->pipe[i], h->ev[0], 0));
+  // context table once per pipe stream (tiny)
+  std::vector<Stage*> stages;
+  int rc = EB_OK;
+  eb_context* d_ctx[3] = {nullptr, nullptr, nullptr};
+  for (int c = 0; c < nchunks && rc == EB_OK; ++c) {
+    cudaStream_t st = h->pipe[c % 3];
+    Stage* S = new Stage(h, st);
+    stages.push_back(S);
+    if (!d_ctx[c % 3]) d_ctx[c % 3] = S->up(ctxs, (size_t)n_ctx);
+    const int64_t i0 = c * chunk, i1 = (i0 + chunk < n) ? i0 + chunk : n, ni = i1 - i0;
+    const int64_t R0 = offsets[i0], R1 = offsets[i1], nr = R1 - R0;
+    const int64_t* d_off = S->up(offsets + i0, (size_t)ni + 1);
+    const int32_t* d_ci = ctx_index ? S->up(ctx_index + i0, (size_t)ni) : nullptr;
+    eb_requests d_req = upload(*S, R0, nr);
+    eb_dftsp_result d_out;
+    memset(&d_out, 0, sizeof(d_out));
+    d_out.status = S->alloc<int32_t>(ni);
+    d_out.error_index = S->out(out.error_index, ni);
+    d_out.z_found = S->alloc<int32_t>(ni);
+    d_out.nodes_visited = S->alloc<int64_t>(ni);
+    d_out.nodes_pruned = S->alloc<int64_t>(ni);
+    d_out.n_classes = S->out(out.n_classes, ni);
+    d_out.counts = S->out(out.counts, ni * EB_MAX_CLASSES);
+    d_out.class_lengths = S->out(out.class_lengths, ni * EB_MAX_CLASSES);
+    d_out.solution = S->out(out.solution, nr);
+    d_out.metrics = S->out(out.metrics, ni * EB_N_METRICS);
+    int64_t T0 = 0;
+    if (prm.collect_trajectory) {
+      T0 = out.traj_offsets[i0];
+      int64_t nt = out.traj_offsets[i1] - T0;
+      d_out.traj_offsets = S->up(out.traj_offsets + i0, (size_t)ni + 1);
+      d_out.traj = S->alloc<int64_t>((size_t)nt * 4);
+      d_out.traj_len = S->out(out.traj_len, ni);
+    }
+    int* d_counter = S->alloc<int>(2);
+    if (S->err) { rc = S->err; break; }
+    rc = launch_dftsp(h, st, d_ctx[c % 3], n_ctx, prm, ni, d_off, d_ci, R0, d_req, K, d_out, T0, d_counter, n_wide);
+    if (rc) break;
+    S->down(out.status + i0, d_out.status, ni);
+    S->down(out.error_index ? out.error_index + i0 : nullptr, d_out.error_index, ni);
+    S->down(out.z_found + i0, d_out.z_found, ni);
+    S->down(out.nodes_visited + i0, d_out.nodes_visited, ni);
+    S->down(out.nodes_pruned + i0, d_out.nodes_pruned, ni);
+    S->down(out.n_classes ? out.n_classes + i0 : nullptr, d_out.n_classes, ni);
+    S->down(out.counts ? out.counts + i0 * EB_MAX_CLASSES : nullptr, d_out.counts, ni * EB_MAX_CLASSES);
+    S->down(out.class_lengths ? out.class_lengths + i0 * EB_MAX_CLASSES : nullptr, d_out.class_lengths,
+            ni * EB_MAX_CLASSES);
+    S->down(out.solution ? out.solution + R0 : nullptr, d_out.solution, nr);
+    S->down(out.metrics ? out.metrics + i0 * EB_N_METRICS : nullptr, d_out.metrics, ni * EB_N_METRICS);
+    if (prm.collect_trajectory) {
+      S->down(out.traj + 4 * T0, d_out.traj, (out.traj_offsets[i1] - T0) * 4);
+      S->down(out.traj_len ? out.traj_len + i0 : nullptr, d_out.traj_len, ni);
+    }
+    if (S->err) { rc = S->err; break; }
+  }
+  for (Stage* S : stages) {
+    int s2 = S->sync();
+    if (!rc) rc = s2;
+  }
+  for (Stage* S : stages) delete S;   // stream-ordered frees
+  for (int i = 0; i < 3; ++i) {
+    cudaEventRecord(h->ev[i], h->pipe[i]);
+    cudaStreamWaitEvent(h->stream, h->ev[i], 0);
+  }
+  for (int i = 0; i < 3; ++i) cudaStreamSynchronize(h->pipe[i]);
+  return rc;
+}
+
 
 }  // namespace
 }  // namespace eb
@@ -283,80 +415,27 @@ int32_t eb_dftsp_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, cons
   }
   if (K > EB_MAX_K_DFTSP) K = EB_MAX_K_DFTSP;
   if (K < 1) K = 1;
-  // Chunking: ~8 chunks for big batches, never below 8192 instances.
-  int64_t chunk = (n + 7) / 8;
-  if (chunk < 8192) chunk = 8192;
-  const int nchunks = (int)((n + chunk - 1) / chunk);
-  // The pipeline streams fork from / join back into the handle's stream so
-  // events a caller records on that stream bracket the whole host->host call.
-  EB_CUDA(cudaEventRecord(h->ev[0], h->stream));
-  for (int i = 0; i < 3; ++i) EB_CUDA(cudaStreamWaitEvent(h->pipe[i], h->ev[0], 0));
-  // context table once per pipe stream (tiny)
-  std::vector<Stage*> stages;
-  int rc = EB_OK;
-  eb_context* d_ctx[3] = {nullptr, nullptr, nullptr};
-  for (int c = 0; c < nchunks && rc == EB_OK; ++c) {
-    cudaStream_t st = h->pipe[c % 3];
-    Stage* S = new Stage(h, st);
-    stages.push_back(S);
-    if (!d_ctx[c % 3]) d_ctx[c % 3] = S->up(ctxs, (size_t)n_ctx);
-    const int64_t i0 = c * chunk, i1 = (i0 + chunk < n) ? i0 + chunk : n, ni = i1 - i0;
-    const int64_t R0 = b->offsets[i0], R1 = b->offsets[i1], nr = R1 - R0;
-    const int64_t* d_off = S->up(b->offsets + i0, (size_t)ni + 1);
-    const int32_t* d_ci = b->ctx_index ? S->up(b->ctx_index + i0, (size_t)ni) : nullptr;
-    eb_requests d_req = upload_req(*S, b->req, R0, nr);
-    eb_dftsp_result d_out;
-    memset(&d_out, 0, sizeof(d_out));
-    d_out.status = S->alloc<int32_t>(ni);
-    d_out.error_index = S->out(out->error_index, ni);
-    d_out.z_found = S->alloc<int32_t>(ni);
-    d_out.nodes_visited = S->alloc<int64_t>(ni);
-    d_out.nodes_pruned = S->alloc<int64_t>(ni);
-    d_out.n_classes = S->out(out->n_classes, ni);
-    d_out.counts = S->out(out->counts, ni * EB_MAX_CLASSES);
-    d_out.class_lengths = S->out(out->class_lengths, ni * EB_MAX_CLASSES);
-    d_out.solution = S->out(out->solution, nr);
-    d_out.metrics = S->out(out->metrics, ni * EB_N_METRICS);
-    int64_t T0 = 0;
-    if (prm->collect_trajectory) {
-      T0 = out->traj_offsets[i0];
-      int64_t nt = out->traj_offsets[i1] - T0;
-      d_out.traj_offsets = S->up(out->traj_offsets + i0, (size_t)ni + 1);
-      d_out.traj = S->alloc<int64_t>((size_t)nt * 4);
-      d_out.traj_len = S->out(out->traj_len, ni);
-    }
-    int* d_counter = S->alloc<int>(2);
-    if (S->err) { rc = S->err; break; }
-    rc = launch_dftsp(h, st, d_ctx[c % 3], n_ctx, *prm, ni, d_off, d_ci, R0, d_req, K, d_out, T0, d_counter, n_wide);
-    if (rc) break;
-    S->down(out->status + i0, d_out.status, ni);
-    S->down(out->error_index ? out->error_index + i0 : nullptr, d_out.error_index, ni);
-    S->down(out->z_found + i0, d_out.z_found, ni);
-    S->down(out->nodes_visited + i0, d_out.nodes_visited, ni);
-    S->down(out->nodes_pruned + i0, d_out.nodes_pruned, ni);
-    S->down(out->n_classes ? out->n_classes + i0 : nullptr, d_out.n_classes, ni);
-    S->down(out->counts ? out->counts + i0 * EB_MAX_CLASSES : nullptr, d_out.counts, ni * EB_MAX_CLASSES);
-    S->down(out->class_lengths ? out->class_lengths + i0 * EB_MAX_CLASSES : nullptr, d_out.class_lengths,
-            ni * EB_MAX_CLASSES);
-    S->down(out->solution ? out->solution + R0 : nullptr, d_out.solution, nr);
-    S->down(out->metrics ? out->metrics + i0 * EB_N_METRICS : nullptr, d_out.metrics, ni * EB_N_METRICS);
-    if (prm->collect_trajectory) {
-      S->down(out->traj + 4 * T0, d_out.traj, (out->traj_offsets[i1] - T0) * 4);
-      S->down(out->traj_len ? out->traj_len + i0 : nullptr, d_out.traj_len, ni);
-    }
-    if (S->err) { rc = S->err; break; }
-  }
-  for (Stage* S : stages) {
-    int s2 = S->sync();
-    if (!rc) rc = s2;
-  }
-  for (Stage* S : stages) delete S;   // stream-ordered frees
-  for (int i = 0; i < 3; ++i) {
-    cudaEventRecord(h->ev[i], h->pipe[i]);
-    cudaStreamWaitEvent(h->stream, h->ev[i], 0);
-  }
-  for (int i = 0; i < 3; ++i) cudaStreamSynchronize(h->pipe[i]);
-  return rc;
+  return dftsp_host_pipeline(h, ctxs, n_ctx, *prm, n, b->offsets, b->ctx_index, K, n_wide, *out,
+                             [&](Stage& S, int64_t R0, int64_t nr) { return upload_req(S, b->req, R0, nr); });
+}
+
+int32_t eb_dftsp_batch_packed(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_search_params* prm,
+                              const eb_batch_packed* b, eb_dftsp_result* out, int32_t mem) {
+  if (!h || !ctxs || n_ctx < 1 || !prm || !b || !out || !out->status || !out->z_found ||
+      !out->nodes_visited || !out->nodes_pruned || b->n_inst < 0 || !b->offsets)
+    return EB_ERR_INVALID_ARG;
+  if (prm->ladder_len < 0 || prm->ladder_len > EB_MAX_CLASSES) return EB_ERR_INVALID_ARG;
+  const eb_requests_packed& r = b->req;
+  if (!r.id || !r.prompt_tokens || !r.output_tokens || !r.deadline_s || !r.waiting_s || !r.channel_gain ||
+      !r.uplink_power_w)
+    return EB_ERR_INVALID_ARG;
+  if (prm->collect_trajectory && (!out->traj || !out->traj_offsets)) return EB_ERR_INVALID_ARG;
+  if (mem != EB_MEM_HOST) return EB_ERR_INVALID_ARG;
+  if (b->k_max < 1 || b->k_max > EB_MAX_K) return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  if (b->n_inst == 0) return EB_OK;
+  return dftsp_host_pipeline(h, ctxs, n_ctx, *prm, b->n_inst, b->offsets, b->ctx_index, b->k_max, 0, *out,
+                             [&](Stage& S, int64_t R0, int64_t nr) { return upload_wire(S, r, R0, nr); });
 }
 
 int32_t eb_dfs_single(eb_handle* h, int32_t z, int32_t n_cls, const int32_t* sizes, const int32_t* lengths,

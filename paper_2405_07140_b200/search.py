@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _lib
 from .feasibility import raise_for_status
-from .soa import InstanceBatch, context_record, search_params
+from .soa import InstanceBatch, WireBatch, context_record, search_params
 
 __all__ = ["ClassPartition", "SearchOutcome", "SearchTables", "partition", "recover_subset", "dfs", "dftsp",
            "exhaustive_optimal", "dftsp_many", "solve_batch", "BatchResult", "exhaustive_many"]
@@ -193,7 +193,7 @@ class BatchResult:
     traj_len: np.ndarray | None = None
 
 
-def solve_batch(batch: InstanceBatch, *, pruning=True, inclusive_bound=False, exact_tau=False,
+def solve_batch(batch: InstanceBatch | WireBatch, *, pruning=True, inclusive_bound=False, exact_tau=False,
                 collect_trajectory=False, ladder=None, device=None, handle=None, algorithm=0,
                 exhaustive_counts=False) -> BatchResult:
     """K3 over a host InstanceBatch: every instance is one dftsp() call.
@@ -225,6 +225,10 @@ def solve_batch(batch: InstanceBatch, *, pruning=True, inclusive_bound=False, ex
                         exhaustive_counts)
     h = handle or _lib.handle(device)
     b = batch.struct()
+    if isinstance(batch, WireBatch):        # compact wire format (eb_dftsp_batch_packed)
+        _lib.check(h.lib.eb_dftsp_batch_packed(h.ptr, batch.contexts.ctypes.data, len(batch.contexts), _ref(prm),
+                                               _ref(b), _ref(out), _lib.EB_MEM_HOST), "eb_dftsp_batch_packed")
+        return res
     _lib.check(h.lib.eb_dftsp_batch(h.ptr, batch.contexts.ctypes.data, len(batch.contexts), _ref(prm), _ref(b),
                                     _ref(out), _lib.EB_MEM_HOST), "eb_dftsp_batch")
     return res

@@ -138,6 +138,89 @@ class InstanceBatch:
         return cls(offsets, cols, contexts, ci, max(sizes) if sizes else 1)
 
 
+# The compact wire format of eb_dftsp_batch_packed (include/edgebatch_b200.h):
+# id int32, token counts uint16, uplink power one value when uniform.
+WIRE_FIELDS = (("id", np.int32), ("prompt_tokens", np.uint16), ("output_tokens", np.uint16),
+               ("deadline_s", np.float64), ("waiting_s", np.float64), ("channel_gain", np.float64))
+
+
+@dataclass
+class WireBatch:
+    """An InstanceBatch in the compact wire format (host arrays only)."""
+
+    offsets: np.ndarray
+    columns: dict
+    uplink_power_w: np.ndarray      # one value (uniform) or one per request
+    contexts: np.ndarray
+    ctx_index: object = None
+    k_max: int = 0
+
+    @property
+    def n_inst(self) -> int:
+        return int(self.offsets.shape[0]) - 1
+
+    @property
+    def n_req(self) -> int:
+        return int(self.columns["prompt_tokens"].shape[0])
+
+    @property
+    def uniform_power(self) -> bool:
+        return self.uplink_power_w.shape[0] == 1
+
+    def nbytes(self) -> int:
+        """Bytes one host->device pass of this batch moves."""
+        n = sum(int(a.nbytes) for a in self.columns.values()) + int(self.uplink_power_w.nbytes)
+        n += int(self.offsets.nbytes)
+        if self.ctx_index is not None:
+            n += int(self.ctx_index.nbytes)
+        return n
+
+    def struct(self) -> "_lib.eb_batch_packed":
+        r = _lib.eb_requests_packed()
+        for name, _ in WIRE_FIELDS:
+            setattr(r, name, ptr(self.columns[name]))
+        r.uplink_power_w = ptr(self.uplink_power_w)
+        r.uplink_power_uniform = int(self.uniform_power)
+        b = _lib.eb_batch_packed()
+        b.n_inst = self.n_inst
+        b.n_req = self.n_req
+        b.offsets = ptr(self.offsets)
+        b.ctx_index = ptr(self.ctx_index)
+        b.req = r
+        b.k_max = int(self.k_max)
+        b._keep = self
+        return b
+
+
+def pack_wire(batch: InstanceBatch, pin=None) -> WireBatch | None:
+    """The wire-format copy of a host batch, or None when a column does not
+    narrow losslessly (ids outside int32, token counts outside uint16) or an
+    instance is wider than EB_MAX_K.  ``pin`` (e.g. ``lambda a:
+    torch.from_numpy(a).pin_memory().numpy()``) places the arrays in pinned
+    memory."""
+    cols = batch.columns
+    if batch.n_inst and int(np.diff(batch.offsets).max()) > _lib.EB_MAX_K:
+        return None
+    ids, pt, ot = cols["id"], cols["prompt_tokens"], cols["output_tokens"]
+    if ids.size and (ids.min() < -2**31 or ids.max() > INT32_MAX):
+        return None
+    for a in (pt, ot):
+        if a.size and (a.min() < 0 or a.max() > 0xFFFF):
+            return None
+    out = {name: np.ascontiguousarray(cols[name], dtype=dt) for name, dt in WIRE_FIELDS}
+    pw = np.ascontiguousarray(cols["uplink_power_w"], dtype=np.float64)
+    if pw.size and (pw.view(np.int64) == pw[:1].view(np.int64)).all():    # same bits: uniform
+        pw = pw[:1].copy()
+    off = np.ascontiguousarray(batch.offsets, dtype=np.int64)
+    ci = None if batch.ctx_index is None else np.ascontiguousarray(batch.ctx_index, dtype=np.int32)
+    if pin is not None:
+        out = {k: pin(v) for k, v in out.items()}
+        pw, off = pin(pw), pin(off)
+        ci = None if ci is None else pin(ci)
+    k = int(batch.k_max) if batch.k_max else (int(np.diff(off).max()) if batch.n_inst else 1)
+    return WireBatch(off, out, pw, batch.contexts, ci, max(1, k))
+
+
 def search_params(pruning=True, inclusive_bound=False, exact_tau=False, collect_trajectory=False, ladder=None,
                   algorithm=0, exhaustive_counts=False):
     p = _lib.eb_search_params()

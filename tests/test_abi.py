@@ -63,6 +63,50 @@ def test_struct_layouts_match_c(tmp_path):
     assert got == want
 
 
+def test_packed_struct_layouts_match_c(tmp_path):
+    gcc = shutil.which("gcc")
+    if not gcc:
+        pytest.skip("gcc missing")
+    src = tmp_path / "lay2.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "edgebatch_b200.h"\n'
+                   'int main(){printf("%zu %zu %zu %zu\\n", sizeof(eb_requests_packed), sizeof(eb_batch_packed),'
+                   ' offsetof(eb_requests_packed, uplink_power_uniform), offsetof(eb_batch_packed, k_max));'
+                   'return 0;}\n')
+    exe = tmp_path / "lay2"
+    subprocess.run([gcc, "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
+    want = [ctypes.sizeof(_lib.eb_requests_packed), ctypes.sizeof(_lib.eb_batch_packed),
+            _lib.eb_requests_packed.uplink_power_uniform.offset, _lib.eb_batch_packed.k_max.offset]
+    assert got == want
+
+
+def test_pack_wire_is_lossless_or_refuses():
+    """Host logic of the wire format: values round-trip exactly; columns that
+    do not narrow losslessly make pack_wire refuse (the caller keeps the wide call)."""
+    import numpy as np
+    from gen_random import random_batch
+    from paper_2405_07140_b200.soa import pack_wire
+    batch, _ = random_batch(5, 200)
+    w = pack_wire(batch)
+    assert w is not None and w.uniform_power
+    for name in ("id", "prompt_tokens", "output_tokens"):
+        assert np.array_equal(w.columns[name].astype(np.int64), batch.columns[name].astype(np.int64))
+    for name in ("deadline_s", "waiting_s", "channel_gain"):
+        assert w.columns[name].tobytes() == batch.columns[name].tobytes()
+    assert w.nbytes() < sum(batch.columns[k].nbytes for k in batch.columns if k != "tolerance")
+    cols = dict(batch.columns)
+    cols["uplink_power_w"] = cols["uplink_power_w"].copy()
+    cols["uplink_power_w"][3] *= 2
+    b2 = type(batch)(batch.offsets, cols, batch.contexts, batch.ctx_index, batch.k_max)
+    w2 = pack_wire(b2)
+    assert not w2.uniform_power and w2.uplink_power_w.tobytes() == cols["uplink_power_w"].tobytes()
+    for name, bad in (("id", 2**31), ("prompt_tokens", 70000), ("output_tokens", -1)):
+        c3 = dict(batch.columns)
+        c3[name] = c3[name].copy()
+        c3[name][0] = bad
+        assert pack_wire(type(batch)(batch.offsets, c3, batch.contexts, batch.ctx_index, batch.k_max)) is None
+
+
 def test_no_gpu_means_loud_failure():
     """Without a device the product raises -- there is no CPU fallback."""
     import torch

@@ -215,3 +215,23 @@ def test_gpu_over_wide_limit_is_k_too_large():
     batch, _ = random_batch(63, 2, k_min=256, k_max=256, max_classes=3)
     dev = search.solve_batch(batch, ladder=None)
     assert (dev.status == _lib.ERR_K_TOO_LARGE).all()
+
+
+@pytest.mark.parametrize("uniform", [True, False])
+def test_gpu_wire_format_matches_wide_call(uniform):
+    """eb_dftsp_batch_packed returns exactly what eb_dftsp_batch returns (and
+    what the oracle returns) on the same instances."""
+    from paper_2405_07140_b200.soa import pack_wire
+    batch, ladders = random_batch(4242 + uniform, 3000, k_max=20)
+    if not uniform:
+        rng = np.random.default_rng(9)
+        batch.columns["uplink_power_w"] = batch.columns["uplink_power_w"] * rng.uniform(0.5, 2.0, batch.n_req)
+    for lad, (idx, sb) in group_by_ladder(batch, ladders).items():
+        w = pack_wire(sb)
+        assert w is not None and w.uniform_power == uniform
+        dev = search.solve_batch(sb, ladder=lad)
+        wire = search.solve_batch(w, ladder=lad)
+        for k in RES_KEYS + ("solution", "metrics", "error_index"):
+            assert np.array_equal(getattr(dev, k), getattr(wire, k)), (lad, k)
+        orc = oracle.dftsp_batch(sb, ladder=lad, threads=8)
+        _assert_same(wire, orc, sb, f"wire ladder {lad}")
