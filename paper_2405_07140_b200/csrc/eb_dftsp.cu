@@ -323,11 +323,12 @@ __device__ __forceinline__ void warp_prefix1(int n, ValFn val, StoreFn store) {
 }
 
 // Full-traversal node counts of one dfs level (dftsp.py:183-234) entered at
-// level k with remaining target r >= 1: (visited, pruned).  PF* = prefix
-// sums over r of F(k+1, .) (index r, F(., 0) = 0).
-template <bool PRUNE, bool INCL, typename PT>
-__device__ __forceinline__ void level_counts(const LevelInfo& li, bool last, int r, const PT* PFV, const PT* PFP,
-                                             uint64_t& fv, uint64_t& fp) {
+// level k with remaining target r >= 1: (visited, pruned).  pf(q, v, p)
+// returns the prefix sums over r' = 1..q of F(k+1, r') (q >= 0, 0 at q = 0):
+// a table lookup, or the closed form of the deepest level.
+template <bool PRUNE, bool INCL, typename PFN>
+__device__ __forceinline__ void level_counts_f(const LevelInfo& li, bool last, int r, PFN pf, uint64_t& fv,
+                                               uint64_t& fp) {
   const int s = li.size, cap = li.tail_next + (INCL ? li.size : 0);
   const int x0 = min(r, s);
   const int xs = PRUNE ? max(0, r - cap) : 0;          // lowest unpruned count
@@ -345,9 +346,21 @@ __device__ __forceinline__ void level_counts(const LevelInfo& li, bool last, int
   fp = (PRUNE && xs > 0) ? (uint64_t)xs : 0;            // prune event at x = xs - 1
   const int xb = (x0 == r) ? x0 - 1 : x0;               // descending nodes x = xb .. xs
   if (xb >= xs) {
-    fv += (uint64_t)(PFV[r - xs] - PFV[r - xb - 1]);
-    fp += (uint64_t)(PFP[r - xs] - PFP[r - xb - 1]);
+    uint64_t hv, hp, lv, lp;
+    pf(r - xs, hv, hp);
+    pf(r - xb - 1, lv, lp);
+    fv += hv - lv;
+    fp += hp - lp;
   }
+}
+
+template <bool PRUNE, bool INCL, typename PT>
+__device__ __forceinline__ void level_counts(const LevelInfo& li, bool last, int r, const PT* PFV, const PT* PFP,
+                                             uint64_t& fv, uint64_t& fp) {
+  level_counts_f<PRUNE, INCL>(li, last, r, [&](int q, uint64_t& v, uint64_t& p) {
+    v = (uint64_t)PFV[q];
+    p = (uint64_t)PFP[q];
+  }, fv, fp);
 }
 
 // Phase barrier of the lockstep (ALGO 2) kernel: every warp of the block
@@ -374,8 +387,9 @@ struct CountsMode {
 // Prefix sums over r of the deepest level's counts (F(m-1, r) is a leaf,
 // dead end or prune; see level_counts), in closed form.
 template <bool PRUNE, bool INCL>
-__device__ __forceinline__ void last_level_prefix(uint64_t s, uint64_t rr, uint64_t& v, uint64_t& p) {
-  const uint64_t t = rr < s ? rr : s;
+__device__ __forceinline__ void last_level_prefix(uint32_t s, uint32_t rr, uint64_t& v, uint64_t& p) {
+  // s, rr <= EB_MAX_K_DFTSP + 1, so every product below fits 32 bits
+  const uint32_t t = rr < s ? rr : s;
   if (PRUNE && !INCL) {            // r <= s: (1, r); r > s: (0, s + 1)
     v = t;
     p = t * (t + 1) / 2 + (rr - t) * (s + 1);
@@ -383,7 +397,7 @@ __device__ __forceinline__ void last_level_prefix(uint64_t s, uint64_t rr, uint6
     v = t + t * (t + 1) / 2 + (rr - t) * (1 + s);
     p = 0;
   } else {                         // inclusive: r <= s: 1 + r; s < r <= 2s: 1 + s; r > 2s: prune s + 1
-    const uint64_t u = rr < 2 * s ? rr : 2 * s;
+    const uint32_t u = rr < 2 * s ? rr : 2 * s;
     v = t + t * (t + 1) / 2 + (u - t) * (1 + s);
     p = (rr - u) * (s + 1);
   }
@@ -653,48 +667,61 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
       uint32_t* RV = rows + (size_t)lane * W2;
       uint32_t* RP = RV + (n + 1);
-      if (m >= 2) {
-        const uint64_t sl = row[m - 1].size;
-        for (int r = 0; r <= d; ++r) {
-          uint64_t v, p;
-          last_level_prefix<PRUNE, INCL>(sl, (uint64_t)r, v, p);
-          ovf |= (v | p) > 0x7fffffffULL;
-          RV[r] = (uint32_t)v;
-          RP[r] = (uint32_t)p;
+      // deepest level in closed form; level m-2 against it, fused with its
+      // running prefix; levels m-3 .. 1 in place over the u32 row (F(k, r)
+      // reads PF_{k+1} only at indices <= r, so r descends, then a prefix).
+      // Prefix sums are monotone, so checking the last one bounds the row.
+      const uint32_t sl = row[m - 1].size;
+      auto pf_last = [&](int q, uint64_t& v, uint64_t& p) { last_level_prefix<PRUNE, INCL>(sl, (uint32_t)q, v, p); };
+      auto pf_row = [&](int q, uint64_t& v, uint64_t& p) { v = RV[q]; p = RP[q]; };
+      if (m >= 3) {
+        const LevelInfo li = row[m - 2];
+        uint64_t av = 0, ap = 0;
+        RV[0] = RP[0] = 0;
+        for (int r = 1; r <= d; ++r) {
+          uint64_t fv, fp;
+          level_counts_f<PRUNE, INCL>(li, false, r, pf_last, fv, fp);
+          av += fv;
+          ap += fp;
+          RV[r] = (uint32_t)av;
+          RP[r] = (uint32_t)ap;
         }
-        for (int k = m - 2; k >= 1; --k) {
-          const LevelInfo li = row[k];
+        ovf |= (av | ap) > 0x7fffffffULL;
+        for (int k = m - 3; k >= 1; --k) {
+          const LevelInfo lk = row[k];
           for (int r = d; r >= 1; --r) {
             uint64_t fv, fp;
-            level_counts<PRUNE, INCL>(li, false, r, RV, RP, fv, fp);
-            ovf |= (fv | fp) > 0x7fffffffULL;
+            level_counts_f<PRUNE, INCL>(lk, false, r, pf_row, fv, fp);
             RV[r] = (uint32_t)fv;
             RP[r] = (uint32_t)fp;
           }
-          uint64_t av = 0, ap = 0;
+          uint64_t bv = 0, bp = 0;
           for (int r = 1; r <= d; ++r) {
-            av += RV[r];
-            ap += RP[r];
-            ovf |= (av | ap) > 0x7fffffffULL;
-            RV[r] = (uint32_t)av;
-            RP[r] = (uint32_t)ap;
+            bv += RV[r];
+            bp += RP[r];
+            RV[r] = (uint32_t)bv;
+            RP[r] = (uint32_t)bp;
           }
-          RV[0] = RP[0] = 0;
+          ovf |= (bv | bp) > 0x7fffffffULL;
         }
       }
       const LevelInfo l0 = row[0];
-      for (int r = found ? zf : 1; r <= d; ++r) {
-        if (found && r == zf && d > dwin) continue;                // after the winning call
-        uint64_t fv, fp;
-        level_counts<PRUNE, INCL>(l0, m == 1, r, RV, RP, fv, fp);
-        fv += 1;                                                   // the root
-        my_v += fv;
-        my_p += fp;
-        if (traj) {
-          int64_t* tr = traj + 4 * (int64_t)((n - r) * (n - r + 1) / 2 + (d - r));
-          tr[0] = r; tr[1] = d; tr[2] = (int64_t)fv; tr[3] = (int64_t)fp;
+      auto level0 = [&](auto pf) {
+        for (int r = found ? zf : 1; r <= d; ++r) {
+          if (found && r == zf && d > dwin) continue;                // after the winning call
+          uint64_t fv, fp;
+          level_counts_f<PRUNE, INCL>(l0, m == 1, r, pf, fv, fp);
+          fv += 1;                                                   // the root
+          my_v += fv;
+          my_p += fp;
+          if (traj) {
+            int64_t* tr = traj + 4 * (int64_t)((n - r) * (n - r + 1) / 2 + (d - r));
+            tr[0] = r; tr[1] = d; tr[2] = (int64_t)fv; tr[3] = (int64_t)fp;
+          }
         }
-      }
+      };
+      if (m >= 3) level0(pf_row);
+      else level0(pf_last);                                          // m == 2 (m == 1 never reads pf)
     }
     if (__any_sync(EB_FULL, ovf)) return false;                    // exact literal-walk pass instead
     __syncwarp();
@@ -713,7 +740,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       if (last) {
         for (int r = lane; r <= n; r += 32) {
           uint64_t v, p;
-          last_level_prefix<PRUNE, INCL>(li.size, (uint64_t)r, v, p);
+          last_level_prefix<PRUNE, INCL>(li.size, (uint32_t)r, v, p);
           KV[r] = v;
           KP[r] = p;
         }
@@ -1411,7 +1438,13 @@ __global__ void __launch_bounds__(32, 1) dftsp_wide_kernel(DftspArgs A, unsigned
 // Lockstep variant (leaf-parallel algorithm): the block takes one instance
 // per warp per round and all warps cross the same phase barriers.
 template <bool PRUNE, bool INCL, bool EXACT, int NI>
-__global__ void __launch_bounds__(512, 1) dftsp_lock_kernel(DftspArgs A) {
+#ifndef EB_LOCK_THREADS
+#define EB_LOCK_THREADS 512
+#endif
+#ifndef EB_LOCK_MINB
+#define EB_LOCK_MINB 1
+#endif
+__global__ void __launch_bounds__(EB_LOCK_THREADS, EB_LOCK_MINB) dftsp_lock_kernel(DftspArgs A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   __shared__ int s_base;
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
