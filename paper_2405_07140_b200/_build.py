@@ -50,8 +50,12 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
 
+    headers = [d for d in deps if not d.endswith(".cu")]
+
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        if not force and not _stale(obj, [src, *headers]):
+            return obj, subprocess.CompletedProcess([], 0, "", "")
         return obj, subprocess.run([_nvcc(), *flags, "-c", "-o", obj, src], capture_output=True, text=True)
 
     # one nvcc per translation unit, in parallel (eb_dftsp.cu dominates)

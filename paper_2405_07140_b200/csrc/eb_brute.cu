@@ -162,13 +162,41 @@ __device__ __forceinline__ bool feasible(const Members& S, int z, const uint8_t*
   return true;
 }
 
+// A prefix idx[0..p) of a size-z combination cannot be completed into a
+// subset that passes check_direct.  Every check_direct quantity is monotone
+// in the member set: the uplink/downlink folds only grow when terms are
+// appended (IEEE addition of a non-negative term is monotone and never
+// decreases the sum), memory and FLOPs are exact integer sums, and the
+// compute time only grows with FLOPs.  So the completion's sums are at least
+// the prefix sums plus the c = z - p smallest terms of the pool (lo_*[c]).
+// The integer bounds are exact; the float bounds on lookahead terms carry the
+// fails_margin slack.  `tight` is the prefix member with the least
+// deadline slack seen so far: it must meet its deadline under the lower
+// bound of the compute time.
+__device__ __forceinline__ bool prefix_infeasible(const Members& S, int z, int p, double pu, double pd,
+                                                  int64_t ps, int64_t pf, int tight) {
+  const int c = z - p;
+  if (!leq(pu, 1.0) || !leq(pd, 1.0)) return true;
+  if (c > 0 && (fails_margin(mul(add(pu, S.lo_a[c]), 0.999999999999), 1.0) ||
+                fails_margin(mul(add(pd, S.lo_b[c]), 0.999999999999), 1.0)))
+    return true;
+  const int64_t mem = S.m1 + S.kvp * z + S.kv * (ps + S.lo_n[c]);
+  if (!leq(mul(S.alpha, i2d(mem)), S.M)) return true;
+  const double cs = div(mul(S.beta, i2d((int64_t)z * S.fi + pf + S.lo_far[c])), S.C);
+  if (S.has_cap && !leq(cs, S.cap_s)) return true;
+  return !leq(add(S.ws[tight], cs), S.dl[tight]);
+}
+
 // Scan ranks [r_lo, r_hi) of level z (lex order) and return the first
 // feasible rank, or -1.  `stop` is polled so a thread quits once an earlier
-// rank is known feasible.
+// rank is known feasible.  Branch and bound over the lexicographic order:
+// when a prefix idx[0..q] cannot be completed (prefix_infeasible), the whole
+// rank range of its completions -- C(n - idx[q] - 1, z - q - 1) ranks, all
+// infeasible -- is skipped, so the first feasible rank is unchanged.
 __device__ int64_t scan_chunk(const Members& S, int z, int64_t r_lo, int64_t r_hi,
                               const unsigned long long* stop) {
   const int n = S.n;
-  uint8_t idx[EB_MAX_K];
+  uint8_t idx[EB_MAX_K], tight[EB_MAX_K + 1];
   double pu[EB_MAX_K + 1], pd[EB_MAX_K + 1];
   int64_t ps[EB_MAX_K + 1], pf[EB_MAX_K + 1];
   // unrank r_lo
@@ -185,23 +213,40 @@ __device__ int64_t scan_chunk(const Members& S, int z, int64_t r_lo, int64_t r_h
   }
   pu[0] = 0.0; pd[0] = 0.0; ps[0] = 0; pf[0] = 0;
   int from = 0;
-  for (int64_t rank = r_lo; rank < r_hi; ++rank) {
+  bool first = true;     // r_lo may sit inside a subtree: no skipping on it
+  int64_t rank = r_lo;
+  int steps = 0;
+  while (rank < r_hi) {
+    int q = z - 1;       // subtree to leave: the full combination (1 rank)
+    bool dead = false;
     for (int j = from; j < z; ++j) {
-      int i = idx[j];
+      const int i = idx[j];
       pu[j + 1] = add(pu[j], S.a[i]);
       pd[j + 1] = add(pd[j], S.b[i]);
       ps[j + 1] = ps[j] + S.nout[i];
       pf[j + 1] = pf[j] + S.far[i];
+      int t = i;
+      if (j > 0) {
+        const int o = tight[j];
+        if (sub(S.dl[o], S.ws[o]) <= sub(S.dl[i], S.ws[i])) t = o;
+      }
+      tight[j + 1] = (uint8_t)t;
+      if (!first && j + 1 < z && prefix_infeasible(S, z, j + 1, pu[j + 1], pd[j + 1], ps[j + 1], pf[j + 1], t)) {
+        q = j;
+        dead = true;
+        break;
+      }
     }
-    if (feasible(S, z, idx, pu[z], pd[z], ps[z], pf[z])) return rank;
-    if (((rank - r_lo) & 255) == 255 && *(volatile const unsigned long long*)stop < (unsigned long long)rank)
-      return -1;
-    // lexicographic successor (itertools.combinations order)
-    int j = z - 1;
+    if (!dead && feasible(S, z, idx, pu[z], pd[z], ps[z], pf[z])) return rank;
+    first = false;
+    rank += (int64_t)binom(n - idx[q] - 1, z - q - 1);
+    if ((++steps & 127) == 0 && *(volatile const unsigned long long*)stop < (unsigned long long)rank) return -1;
+    // successor of the last combination of subtree(idx[0..q])
+    int j = q;
     while (j >= 0 && idx[j] == n - z + j) --j;
     if (j < 0) break;
     idx[j] += 1;
-    for (int q = j + 1; q < z; ++q) idx[q] = idx[q - 1] + 1;
+    for (int q2 = j + 1; q2 < z; ++q2) idx[q2] = idx[q2 - 1] + 1;
     from = j;
   }
   return -1;

@@ -68,3 +68,33 @@ def test_rank_range_sharding_reassembles_the_answer():
         for world in (2, 3, 8):
             got = solve_sharded(b.contexts[ci:ci + 1], cols, world=world)
             assert (got.z, got.lexrank, got.nodes_visited) == (int(z[i]), int(rk[i]), int(nodes[i])), (i, world)
+
+
+@pytest.mark.parametrize("seed", [21, 22, 23, 24])
+def test_branch_and_bound_matches_oracle_many(seed):
+    """The prefix bounds of scan_chunk skip only infeasible rank ranges: the
+    first feasible rank (and so z, rank, nodes, mask) equals the oracle's plain
+    enumeration on many small/medium pools, including tight slot caps."""
+    b, _ = random_batch(seed, 250, k_min=1, k_max=15, slot_cap_frac=0.6)
+    st, z, rk, nodes, mask = _run(b)
+    for i in range(b.n_inst):
+        ci = int(b.ctx_index[i])
+        e = oracle.exhaustive(b.contexts[ci:ci + 1], b.columns, int(b.offsets[i]), int(b.offsets[i + 1]))
+        assert (int(st[i]), int(z[i]), int(rk[i]), int(nodes[i]), int(mask[i])) == e, (seed, i)
+
+
+def test_branch_and_bound_config2_pools():
+    """Config-2 pools (K=20, BLOOM-3B mix): batch kernel and 5-way rank sharding
+    against the oracle's enumeration."""
+    from paper_2405_07140_b200 import synth
+    from paper_2405_07140_b200.brute import solve_sharded
+    b = synth.generate(synth.CONFIG2, 12, seed=77)
+    st, z, rk, nodes, mask = _run(b)
+    for i in range(b.n_inst):
+        ci = int(b.ctx_index[i])
+        lo, hi = int(b.offsets[i]), int(b.offsets[i + 1])
+        e = oracle.exhaustive(b.contexts[ci:ci + 1], b.columns, lo, hi)
+        assert (int(st[i]), int(z[i]), int(rk[i]), int(nodes[i]), int(mask[i])) == e, i
+        cols = {k: np.ascontiguousarray(v[lo:hi]) for k, v in b.columns.items()}
+        got = solve_sharded(b.contexts[ci:ci + 1], cols, world=5)
+        assert (got.z, got.lexrank, got.nodes_visited) == (int(z[i]), int(rk[i]), int(nodes[i])), i
