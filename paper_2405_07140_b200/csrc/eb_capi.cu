@@ -351,6 +351,8 @@ int32_t eb_handle_destroy(eb_handle* h) {
   for (int i = 0; i < 3; ++i) { cudaStreamDestroy(h->pipe[i]); cudaEventDestroy(h->ev[i]); }
   if (h->dscratch) cudaFree(h->dscratch);
   if (h->pinned) cudaFreeHost(h->pinned);
+  for (int i = 0; i < 3; ++i)
+    if (h->ctab[i]) cudaFree(h->ctab[i]);
   delete h;
   return EB_OK;
 }

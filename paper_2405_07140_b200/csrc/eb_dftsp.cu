@@ -99,6 +99,7 @@ struct DftspArgs {
   eb_dftsp_result out;        // per-instance arrays launch-local; solution at row - req_base
   int64_t traj_base;          // absolute row of out.traj element 0
   int* counter;               // [0] instance queue, [1] fallback count
+  const uint2* ctab;          // node-count table for this flag variant (K <= 32), or null
   int fallback_pass;
 };
 
@@ -403,13 +404,75 @@ __device__ __forceinline__ void last_level_prefix(uint32_t s, uint32_t rr, uint6
   }
 }
 
+// Node-count tables for instances of at most 32 requests and at most three
+// output classes.  Per partition shape (m classes of sizes s0, s1, s2, in
+// level order) they hold PF0(q) = sum over r = 1..q of F(0, r) (visited,
+// pruned), the full-traversal counts of dfs calls with target r computed by
+// the same recurrence as search_v2 (level_counts_f / last_level_prefix).
+// Summing F(0, z) over a z range is then two lookups.  Layout (uint2
+// entries): m = 3 at [s0][s1][s2][q], m = 2 at CT^4 + [s0][s1][q], m = 1 at
+// CT^4 + CT^3 + [s0][q].
+constexpr int CT = 33;
+constexpr size_t CT_ENTRIES = (size_t)CT * CT * CT * CT + (size_t)CT * CT * CT + (size_t)CT * CT;
+
+__host__ __device__ __forceinline__ size_t ct_base(int m, int s0, int s1, int s2) {
+  const size_t c3 = (size_t)CT * CT * CT * CT, c2 = (size_t)CT * CT * CT;
+  if (m == 3) return (((size_t)s0 * CT + s1) * CT + s2) * CT;
+  if (m == 2) return c3 + ((size_t)s0 * CT + s1) * CT;
+  return c3 + c2 + (size_t)s0 * CT;
+}
+
+template <bool PRUNE, bool INCL>
+__global__ void count_table_kernel(uint2* T) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n3 = 32 * 32 * 32, n2 = 32 * 32;
+  int m, sz[3] = {0, 0, 0};
+  if (t < n3) { m = 3; sz[0] = 1 + t / 1024; sz[1] = 1 + (t / 32) % 32; sz[2] = 1 + t % 32; }
+  else if (t < n3 + n2) { m = 2; sz[0] = 1 + (t - n3) / 32; sz[1] = 1 + (t - n3) % 32; }
+  else if (t < n3 + n2 + 32) { m = 1; sz[0] = 1 + (t - n3 - n2); }
+  else return;
+  const int d = sz[0] + sz[1] + sz[2];
+  if (d > 32) return;
+  LevelInfo row[3];
+  int tail = 0;
+  for (int k = m - 1; k >= 0; --k) {
+    row[k].off = 0; row[k].size = (uint8_t)sz[k]; row[k].tail_next = (uint8_t)tail; row[k].g = (uint8_t)k;
+    row[k].pad[0] = row[k].pad[1] = row[k].pad[2] = 0;
+    tail += sz[k];
+  }
+  const uint32_t sl = sz[m - 1];
+  auto pf_last = [&](int q, uint64_t& v, uint64_t& p) { last_level_prefix<PRUNE, INCL>(sl, (uint32_t)q, v, p); };
+  uint32_t RV[CT], RP[CT];
+  auto pf_row = [&](int q, uint64_t& v, uint64_t& p) { v = RV[q]; p = RP[q]; };
+  if (m == 3) {                       // level 1 against the closed-form level 2, prefix-summed
+    uint64_t av = 0, ap = 0;
+    RV[0] = RP[0] = 0;
+    for (int r = 1; r <= d; ++r) {
+      uint64_t fv, fp;
+      level_counts_f<PRUNE, INCL>(row[1], false, r, pf_last, fv, fp);
+      av += fv; ap += fp;
+      RV[r] = (uint32_t)av; RP[r] = (uint32_t)ap;
+    }
+  }
+  uint2* out = T + ct_base(m, sz[0], sz[1], sz[2]);
+  uint64_t av = 0, ap = 0;
+  out[0] = make_uint2(0u, 0u);
+  for (int r = 1; r <= d; ++r) {
+    uint64_t fv, fp;
+    if (m == 3) level_counts_f<PRUNE, INCL>(row[0], false, r, pf_row, fv, fp);
+    else level_counts_f<PRUNE, INCL>(row[0], m == 1, r, pf_last, fv, fp);
+    av += fv; ap += fp;
+    out[r] = make_uint2((uint32_t)av, (uint32_t)ap);
+  }
+}
+
 template <bool PRUNE, bool INCL, bool EXACT, int NI>
 __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const Lay& L, const LevelInfo* lvl,
                           const uint8_t* ncls_d, const double* t_up, const double* t_dn, const double* t_tau,
                           const int32_t* c_len, const double* c_w, const double* o_tau, double k2, double k3,
                           double slot_base, bool has_cap, int padded, int64_t* traj, bool& found, int& zf,
                           int& dwin, int& kwin, uint64_t& W0, uint64_t& W1, int& best, uint64_t& tot_v,
-                          uint64_t& tot_p, const CountsMode& cm) {
+                          uint64_t& tot_p, const CountsMode& cm, const uint2* ctab) {
   const int lane = threadIdx.x & 31;
   uint64_t cm_before = 0;   // counts mode: count vectors tried in completed windows
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
@@ -671,6 +734,16 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       // running prefix; levels m-3 .. 1 in place over the u32 row (F(k, r)
       // reads PF_{k+1} only at indices <= r, so r descends, then a prefix).
       // Prefix sums are monotone, so checking the last one bounds the row.
+      if (ctab != nullptr && m <= 3 && !traj) {                     // tabulated shape: two lookups
+        const int lo = found ? (d > dwin ? zf + 1 : zf) : 1;
+        if (lo <= d) {
+          const uint2* T = ctab + ct_base(m, row[0].size, m > 1 ? row[1].size : 0, m > 2 ? row[2].size : 0);
+          const uint2 a = T[d], b = T[lo - 1];
+          my_v += (uint64_t)(a.x - b.x) + (uint64_t)(d - lo + 1);    // + one root per call
+          my_p += (uint64_t)(a.y - b.y);
+        }
+        continue;
+      }
       const uint32_t sl = row[m - 1].size;
       auto pf_last = [&](int q, uint64_t& v, uint64_t& p) { last_level_prefix<PRUNE, INCL>(sl, (uint32_t)q, v, p); };
       auto pf_row = [&](int q, uint64_t& v, uint64_t& p) { v = RV[q]; p = RP[q]; };
@@ -1191,7 +1264,8 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     if (!search_v2<PRUNE, INCL, EXACT, NI>(passed, n, Gi, smem, L, lvl, ncls_d, t_up, t_dn, t_tau, c_len, c_w, o_tau, k2, k3,
                                        slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
                                        tot_v, tot_p,
-                                       CountsMode{A.prm.exhaustive_counts != 0, c_start, c_list, o_key, o_dnt})) {
+                                       CountsMode{A.prm.exhaustive_counts != 0, c_start, c_list, o_key, o_dnt},
+                                       NI == 1 ? A.ctab : nullptr)) {
       // leaf counts overflow the u32 unranking tables: hand the instance to
       // the literal walk (second pass of launch_dftsp)
       put_status(EB_STATUS_FALLBACK, -1);
@@ -1591,6 +1665,7 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   A.ctxs = d_ctxs; A.n_ctx = n_ctx; A.prm = prm; A.n_inst = n_inst; A.offsets = d_off;
   A.ctx_index = d_ctx_index; A.req_base = req_base; A.req = d_req; A.K = K; A.G = G;
   A.out = d_out; A.traj_base = traj_base; A.counter = d_counter; A.fallback_pass = 0;
+  A.ctab = nullptr;
   // algorithm: 2 = leaf-parallel (default) unless its tables do not fit two
   // warps per block, 1 = literal lanes-per-call (also v2's in-kernel fallback)
   int algo = prm.algorithm;
@@ -1643,6 +1718,24 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   }
 #undef EB_PICKL3
   A.fallback_pass = 0;
+  if (algo == 2 && K <= 32 && !prm.exhaustive_counts) {
+    const int v = !P ? 0 : (I ? 2 : 1);
+    if (!h->ctab[v]) {
+      // built once per handle and flag variant; synchronous, so kernels on
+      // the other pipeline streams never see a partial table
+      void* t = nullptr;
+      EB_CUDA(cudaMalloc(&t, CT_ENTRIES * sizeof(uint2)));
+      void (*bk)(uint2*) = !P ? count_table_kernel<false, false>
+                              : (I ? count_table_kernel<true, true> : count_table_kernel<true, false>);
+      const int nthr = 32 * 32 * 32 + 32 * 32 + 32;
+      bk<<<(nthr + 255) / 256, 256, 0, st>>>((uint2*)t);
+      EB_CUDA(cudaGetLastError());
+      h->launches += 1;
+      EB_CUDA(cudaStreamSynchronize(st));
+      h->ctab[v] = t;
+    }
+    A.ctab = (const uint2*)h->ctab[v];
+  }
   EB_CUDA(cudaMemsetAsync(d_counter, 0, 2 * sizeof(int), st));
   int rc = launch_one(h, st, kern, A, warps, smem, n_inst);
   if (rc) return rc;

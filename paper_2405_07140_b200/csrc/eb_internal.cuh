@@ -86,6 +86,10 @@ struct eb_handle {
   size_t dscratch_bytes;
   void* pinned;
   size_t pinned_bytes;
+  // DFTSP node-count tables (K <= 32, <= 3 classes), one per flag variant
+  // (0: pruning off, 1: pruning, 2: pruning + inclusive bound); built on
+  // first use (eb_dftsp.cu count_table_kernel)
+  void* ctab[3];
 };
 
 namespace eb {
