@@ -1190,11 +1190,22 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
 
   // ---------------- per pool width d: class sizes, levels, tables --------
   const int nDG = n * Gi;
-  for (int w = lane; w < nDG; w += 32) {
-    int d = w / Gi + 1, g = w % Gi;
-    int cnt = 0, b = c_start[g], e = c_start[g + 1];
-    for (int q = b; q < e; ++q) cnt += c_list[q] < d;
-    sizes[(d - 1) * Gi + g] = (uint8_t)cnt;
+  if constexpr (NI == 1) {
+    // sizes[d][g] = members of class g among the d first in tau order: one
+    // ballot per class over lanes = tau ranks, then lanes = d count bits < d
+    const int gt = lane < n ? o_g[lane] : -1;
+    const unsigned below = (lane < n) ? ((2u << lane) - 1u) : 0u;     // ranks 0 .. d-1, d = lane + 1
+    for (int g = 0; g < Gi; ++g) {
+      const unsigned mg = __ballot_sync(EB_FULL, gt == g);
+      if (lane < n) sizes[lane * Gi + g] = (uint8_t)__popc(mg & below);
+    }
+  } else {
+    for (int w = lane; w < nDG; w += 32) {
+      int d = w / Gi + 1, g = w % Gi;
+      int cnt = 0, b = c_start[g], e = c_start[g + 1];
+      for (int q = b; q < e; ++q) cnt += c_list[q] < d;
+      sizes[(d - 1) * Gi + g] = (uint8_t)cnt;
+    }
   }
   __syncwarp();
   for (int d = lane + 1; d <= n; d += 32) {
@@ -1367,7 +1378,28 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   if (found) {
     // recover_subset (dftsp.py:85-93) in recover order, then check_direct
     // (feasibility.py:192-223) exactly as dftsp.py:276 calls it.
-    if (lane == 0) {
+    if constexpr (NI == 1) {
+      // lanes = class-list positions p (class-major, within-class key order):
+      // member t = c_list[p] of class g is taken iff t < dwin and fewer than
+      // count[level of g] earlier members of g qualify; its slot is the
+      // counts of earlier levels plus that rank (same order as the loop below)
+      const int t = lane < n ? c_list[lane] : 0;
+      const int g = lane < n ? o_g[t] : 0;
+      const bool in = lane < n && t < dwin;
+      const unsigned inm = __ballot_sync(EB_FULL, in);
+      const unsigned present = __reduce_or_sync(EB_FULL, in ? (1u << g) : 0u);
+      if (in) {
+        const int cs = c_start[g];
+        const int rk = __popc(inm & ((1u << lane) - 1u) & ~((1u << cs) - 1u));
+        const int kk = __popc(present & ((1u << g) - 1u));
+        const int cnt = (kk <= kwin) ? getV(W0, W1, kk) : 0;
+        if (rk < cnt) {
+          int base = 0;
+          for (int k2 = 0; k2 < kk && k2 <= kwin; ++k2) base += getV(W0, W1, k2);
+          sol[base + rk] = (uint8_t)t;
+        }
+      }
+    } else if (lane == 0) {
       int q = 0;
       for (int kk = 0; kk < wncls; ++kk) {
         int cnt = (kk <= kwin) ? getV(W0, W1, kk) : 0;
