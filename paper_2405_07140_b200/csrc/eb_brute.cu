@@ -63,10 +63,7 @@ struct Members {
 // true only if leq(a, b) is false for every a >= a_lo (leq is monotone in a);
 // the margin (1e-5 of the 1e-9 slack) dwarfs any rounding of the bounds.
 __device__ __forceinline__ bool fails_margin(double a_lo, double b) {
-  double m = 1.0;
-  double aa = fabs_(a_lo), ab = fabs_(b);
-  if (aa > m) m = aa;
-  if (ab > m) m = ab;
+  const double m = fmax(fmax(1.0, fabs_(a_lo)), fabs_(b));
   return sub(a_lo, b) > mul(1.00001e-9, m);
 }
 

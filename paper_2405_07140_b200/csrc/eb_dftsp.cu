@@ -100,6 +100,7 @@ struct DftspArgs {
   int64_t traj_base;          // absolute row of out.traj element 0
   int* counter;               // [0] instance queue, [1] fallback count
   const uint2* ctab;          // node-count table for this flag variant (K <= 32), or null
+  Lay lay;                    // per-warp shared-memory layout (make_lay(K, G, exact, algorithm 2))
   int fallback_pass;
 };
 
@@ -262,10 +263,7 @@ __device__ __forceinline__ int dfs_step(Lane& s, const Tables& T) {
 // ===========================================================================
 __device__ __forceinline__ bool fails_with_margin(double a_lo, double b) {
   // true only if leq(a, b) is false for every a >= a_lo (leq is monotone in a)
-  double m = 1.0;
-  double aa = fabs_(a_lo), ab = fabs_(b);
-  if (aa > m) m = aa;
-  if (ab > m) m = ab;
+  const double m = fmax(fmax(1.0, fabs_(a_lo)), fabs_(b));
   return sub(a_lo, b) > mul(1.00001e-9, m);
 }
 
@@ -905,7 +903,7 @@ template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI>
 __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* smem, int& passed) {
   const int lane = threadIdx.x & 31;
   const int K = A.K, G = A.G;
-  const Lay L = make_lay(K, G, EXACT, ALGO == 2);
+  const Lay& L = A.lay;       // computed once on the host (make_lay)
   double* a_tau = (double*)(smem + L.a_tau);
   double* a_key = (double*)(smem + L.a_key);
   int64_t* a_id = (int64_t*)(smem + L.a_id);
@@ -1075,7 +1073,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       if constexpr (NI == 1) {
         for (int j = 0; j < n; ++j) {
           double tj = a_tau[j];
-          t += (tj > tau_i[h]) || (tj == tau_i[h] && a_id[j] < id_i[h]);
+          t += (int)(tj > tau_i[h]) | ((int)(tj == tau_i[h]) & (int)(a_id[j] < id_i[h]));
         }
         first = (peers & lanemask_lt()) == 0;
       } else {
@@ -1131,7 +1129,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
         for (unsigned pm = peers & ~(1u << lane); pm; pm &= pm - 1) {
           const int j = __ffs(pm) - 1;
           const double kj = a_key[j];
-          kr += (kj < key_i[h]) || (kj == key_i[h] && a_id[j] < id_i[h]);
+          kr += (int)(kj < key_i[h]) | ((int)(kj == key_i[h]) & (int)(a_id[j] < id_i[h]));
         }
       } else {
         for (int j = 0; j < n; ++j) {
@@ -1652,7 +1650,8 @@ static int launch_wide(eb_handle* h, cudaStream_t st, const DftspArgs& A0, int K
   W.G = A0.prm.ladder_len > 0 ? A0.prm.ladder_len : (Kw < EB_MAX_CLASSES ? Kw : EB_MAX_CLASSES);
   W.fallback_pass = 0;
   const bool exact = A0.prm.exact_tau != 0;
-  W.warp_bytes = al8(make_lay(Kw, W.G, exact, false).total);
+  W.lay = make_lay(Kw, W.G, exact, false);
+  W.warp_bytes = al8(W.lay.total);
   const size_t smem_cap = 227 * 1024;
   const bool in_smem = W.warp_bytes <= smem_cap;
   int64_t grid = n_wide > 0 ? n_wide : W.n_inst;
@@ -1712,7 +1711,8 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   }
   if (algo != 1 && al8(make_lay(K, G, exact, true).total) * 2 > smem_cap) algo = 1;
   if (algo != 1) algo = 2;
-  A.warp_bytes = al8(make_lay(K, G, exact, algo == 2).total);
+  A.lay = make_lay(K, G, exact, algo == 2);
+  A.warp_bytes = al8(A.lay.total);
   int warps = (int)(smem_cap / A.warp_bytes);
   if (warps > 4) warps = 4;
   if (warps < 1) { set_error("instance size K=%d needs %zu B shared memory per warp", K, A.warp_bytes); return EB_ERR_K_TOO_LARGE; }
@@ -1775,7 +1775,8 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   // literal-walk pass for any instance whose leaf counts overflowed u32
   DftspArgs B = A;
   B.fallback_pass = 1;
-  B.warp_bytes = al8(make_lay(K, G, exact, false).total);
+  B.lay = make_lay(K, G, exact, false);
+  B.warp_bytes = al8(B.lay.total);
   int wb = (int)(smem_cap / B.warp_bytes);
   if (wb > 4) wb = 4;
   EB_PICK(1)

@@ -100,11 +100,10 @@ EB_HD double pymin(double a, double b) { return (b < a) ? b : a; }
 EB_HD double pymax(double a, double b) { return (b > a) ? b : a; }
 
 // feasibility.py:28-30  leq(a, b) = a - b <= 1e-9 * max(1.0, abs(a), abs(b))
+// (fmax drops a NaN operand exactly as the comparison chain of Python's max
+// keeps its current value, so m is the same double.)
 EB_HD bool leq(double a, double b) {
-  double m = 1.0;
-  double aa = fabs_(a), ab = fabs_(b);
-  if (aa > m) m = aa;
-  if (ab > m) m = ab;
+  const double m = fmax(fmax(1.0, fabs_(a)), fabs_(b));
   return sub(a, b) <= mul(1e-9, m);
 }
 
