@@ -197,12 +197,18 @@ template <typename Upload>
 int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const eb_search_params& prm, int64_t n,
                         const int64_t* offsets, const int32_t* ctx_index, int K, int64_t n_wide,
                         const eb_dftsp_result& out, Upload upload) {
-  // Chunking: ~16 chunks for big batches (the first chunk's copy and the
-  // last chunk's search are the exposed pipeline fill), never below 8192
-  // instances.
-  int64_t chunk = (n + 15) / 16;
-  if (chunk < 8192) chunk = 8192;
-  const int nchunks = (int)((n + chunk - 1) / chunk);
+  // Chunking: the first chunk's copy is exposed pipeline fill, so chunks
+  // start at n/64 and double up to n/16 (never below 8192 instances).
+  std::vector<int64_t> cut{0};
+  {
+    const int64_t full = (n + 15) / 16 > 8192 ? (n + 15) / 16 : 8192;
+    int64_t step = n / 64 > 8192 ? n / 64 : 8192;
+    while (cut.back() < n) {
+      cut.push_back(cut.back() + step < n ? cut.back() + step : n);
+      step = step * 2 < full ? step * 2 : full;
+    }
+  }
+  const int nchunks = (int)cut.size() - 1;
   // The pipeline streams fork from / join back into the handle's stream so
   // events a caller records on that stream bracket the whole host->host call.
   EB_CUDA(cudaEventRecord(h->ev[0], h->stream));
@@ -216,7 +222,7 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
     Stage* S = new Stage(h, st);
     stages.push_back(S);
     if (!d_ctx[c % 3]) d_ctx[c % 3] = S->up(ctxs, (size_t)n_ctx);
-    const int64_t i0 = c * chunk, i1 = (i0 + chunk < n) ? i0 + chunk : n, ni = i1 - i0;
+    const int64_t i0 = cut[c], i1 = cut[c + 1], ni = i1 - i0;
     const int64_t R0 = offsets[i0], R1 = offsets[i1], nr = R1 - R0;
     const int64_t* d_off = S->up(offsets + i0, (size_t)ni + 1);
     const int32_t* d_ci = ctx_index ? S->up(ctx_index + i0, (size_t)ni) : nullptr;
