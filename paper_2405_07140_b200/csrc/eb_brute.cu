@@ -266,7 +266,7 @@ struct BatchArgs {
 };
 
 // One block per instance (many small instances).
-__global__ void __launch_bounds__(256) exh_batch_kernel(BatchArgs A) {
+__global__ void __launch_bounds__(256) exh_batch_kernel(const __grid_constant__ BatchArgs A) {
   __shared__ Members S;
   __shared__ unsigned long long best;
   for (int64_t inst = blockIdx.x; inst < A.n_inst; inst += gridDim.x) {
@@ -349,7 +349,7 @@ struct RangeArgs {
 };
 
 // Grid-wide: one level, rank range [lo, hi) split in chunks of `per`.
-__global__ void __launch_bounds__(256) exh_range_kernel(RangeArgs A) {
+__global__ void __launch_bounds__(256) exh_range_kernel(const __grid_constant__ RangeArgs A) {
   __shared__ Members S;
   load_members(S, A.c, A.req, 0, A.n);
   if (S.status) {

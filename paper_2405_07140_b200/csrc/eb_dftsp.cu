@@ -28,6 +28,14 @@
 namespace eb {
 namespace {
 
+#ifdef EB_STATS
+// Debug-only search statistics (a -DEB_STATS build; see tools/search_stats.py).
+__device__ unsigned long long g_stats[16];
+#define EB_STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_stats[i], (unsigned long long)(v)); } while (0)
+#else
+#define EB_STAT(i, v) do { } while (0)
+#endif
+
 constexpr int RING = 64;  // in-flight window of dfs calls per warp
 constexpr int EB_STATUS_FALLBACK = 99;  // internal: v2 tables overflowed, v1 pass pending
 
@@ -383,6 +391,37 @@ struct CountsMode {
   const double* o_dnt;      // k_down * n per tau rank
 };
 
+// SearchTables.build (dftsp.py:110-132) for class g of pool width d: the
+// up / dn (/ tau-min) prefix tables over the class members among the d first
+// in tau order, in within-class key order, at offset base(d) + sum over
+// classes g2 < g of (size + 1).  One lane; the folds are sequential (each
+// prefix is the previous one plus one term, as in the reference).
+template <bool EXACT>
+__device__ __forceinline__ void build_width_tables(int d, int g, int Gi, const uint8_t* sizes, const int32_t* c_start,
+                                                   const uint8_t* c_list, const double* o_key, const double* o_dnt,
+                                                   const double* o_tau, double* t_up, double* t_dn, double* t_tau) {
+  const int base = (d - 1) * d / 2 + (d - 1) * Gi;
+  int start = 0;
+  for (int g2 = 0; g2 < g; ++g2) start += sizes[(d - 1) * Gi + g2] + 1;
+  const int off = base + start;
+  double cu = 0.0, cd = 0.0, tm = __longlong_as_double(0x7ff0000000000000LL);
+  t_up[off] = cu; t_dn[off] = cd;
+  if (EXACT) t_tau[off] = tm;
+  int x = 0;
+  const int b = c_start[g], e = c_start[g + 1];
+  for (int q = b; q < e; ++q) {
+    const int t = c_list[q];
+    if (t < d) {
+      ++x;
+      cu = add(cu, o_key[t]);                    // cu[-1] + k_up*s   (dftsp.py:126)
+      cd = add(cd, o_dnt[t]);                    // cd[-1] + k_down*n (dftsp.py:127)
+      t_up[off + x] = cu;
+      t_dn[off + x] = cd;
+      if (EXACT) { tm = pymin(tm, o_tau[t]); t_tau[off + x] = tm; }  // dftsp.py:128
+    }
+  }
+}
+
 // Prefix sums over r of the deepest level's counts (F(m-1, r) is a leaf,
 // dead end or prune; see level_counts), in closed form.
 template <bool PRUNE, bool INCL>
@@ -470,7 +509,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
                           const int32_t* c_len, const double* c_w, const double* o_tau, double k2, double k3,
                           double slot_base, bool has_cap, int padded, int64_t* traj, bool& found, int& zf,
                           int& dwin, int& kwin, uint64_t& W0, uint64_t& W1, int& best, uint64_t& tot_v,
-                          uint64_t& tot_p, const CountsMode& cm, const uint2* ctab) {
+                          uint64_t& tot_p, const CountsMode& cm, const uint2* ctab, const uint8_t* sizes) {
   const int lane = threadIdx.x & 31;
   uint64_t cm_before = 0;   // counts mode: count vectors tried in completed windows
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
@@ -524,10 +563,12 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
   //      sequence order, 32 per step, first passing leaf wins.
   found = false;
   const int total_calls = n * (n + 1) / 2;
+  EB_STAT(0, 1);
   for (int c0 = 0; c0 < total_calls && !found; c0 += 32) {
     const int c = c0 + lane;
     int z = 0, d = 0;
     bool live = false;
+    EB_STAT(1, 1);
     if (c < total_calls) {
       call_zd(n, c, z, d);
       const double k3z = mul(k3, i2d(z));                            // coeff.k3 * z
@@ -558,10 +599,23 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
                       ((uint64_t)__reduce_or_sync(EB_FULL, (unsigned)(bit >> 32)) << 32);
       want &= ~built;
       bool ok = true;
+      if (want) {
+        // prefix tables of the new widths: lanes = (width, class) pairs
+        const int nwant = __popcll(want);
+        for (int w = lane; w < nwant * Gi; w += 32) {
+          const int wi = w / Gi, g = w % Gi;
+          uint64_t mm = want;
+          for (int q = 0; q < wi; ++q) mm &= mm - 1;               // drop the wi lowest widths
+          build_width_tables<EXACT>(__ffsll((long long)mm), g, Gi, sizes, cm.c_start, cm.c_list, cm.o_key,
+                                    cm.o_dnt, o_tau, (double*)t_up, (double*)t_dn, (double*)t_tau);
+        }
+        __syncwarp();
+      }
       while (want) {
         const int dd = __ffsll((long long)want);
         want &= want - 1;
         ok &= build_pq(dd);
+        EB_STAT(5, 1);
         built |= 1ULL << (dd - 1);
       }
       if (!ok) return false;
@@ -596,6 +650,11 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       if (lane >= o) inc += t;
     }
     const uint32_t T = __shfl_sync(EB_FULL, inc, 31);
+#ifdef EB_STATS
+    { const unsigned lv = __ballot_sync(EB_FULL, live); EB_STAT(6, __popc(lv)); }
+#endif
+    EB_STAT(2, T > 0);
+    EB_STAT(4, T);
     if (T == 0) { cm_before += nall_tot; continue; }
     pre[lane] = inc - cnt;
     pre[32 + lane] = (uint32_t)((z << 8) | d);                      // call of this slot
@@ -603,6 +662,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
     __syncwarp();
     for (uint32_t b0 = 0; b0 < T; b0 += 32) {
       const uint32_t g = b0 + lane;
+      EB_STAT(3, 1);
       bool pass = false;
       int klast = 0, zz = 0, dd = 0, slot = 0;
       uint32_t i0 = 0;
@@ -701,6 +761,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
     __syncwarp();
   }
   best = found ? (n - zf) * (n - zf + 1) / 2 + (dwin - zf) : INT_MAX;
+  EB_STAT(7, found ? best + 1 : total_calls);
 
   phase_barrier<2>(passed);
   if (cm.on) {                       // nodes = count vectors tried; no pruning
@@ -1104,7 +1165,8 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       int i = lane + 32 * h;
       if (i < n) {
         bool ok = false;
-        for (int q = 0; q < A.prm.ladder_len; ++q) ok |= (A.prm.ladder[q] == len_i[h]);
+#pragma unroll
+        for (int q = 0; q < EB_MAX_CLASSES; ++q) ok |= (q < A.prm.ladder_len) & (A.prm.ladder[q] == len_i[h]);
         if (!ok && t_i[h] < bad_t) { bad_t = t_i[h]; bad_i = i; }
       }
     }
@@ -1234,27 +1296,12 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     for (int q = 0; q < k; ++q) if (row[q].g == gn) kn = q;
     row[0].pad[0] = (uint8_t)kn;
   }
-  for (int w = lane; w < nDG; w += 32) {
-    int d = w / Gi + 1, g = w % Gi;
-    int base = (d - 1) * d / 2 + (d - 1) * Gi;
-    int start = 0;
-    for (int g2 = 0; g2 < g; ++g2) start += sizes[(d - 1) * Gi + g2] + 1;
-    int off = base + start;
-    double cu = 0.0, cd = 0.0, tm = __longlong_as_double(0x7ff0000000000000LL);
-    t_up[off] = cu; t_dn[off] = cd;
-    if (EXACT) t_tau[off] = tm;
-    int x = 0, b = c_start[g], e = c_start[g + 1];
-    for (int q = b; q < e; ++q) {
-      int t = c_list[q];
-      if (t < d) {
-        ++x;
-        cu = add(cu, o_key[t]);                    // cu[-1] + k_up*s   (dftsp.py:126)
-        cd = add(cd, o_dnt[t]);                    // cd[-1] + k_down*n (dftsp.py:127)
-        t_up[off + x] = cu;
-        t_dn[off + x] = cd;
-        if (EXACT) { tm = pymin(tm, o_tau[t]); t_tau[off + x] = tm; }  // dftsp.py:128
-      }
-    }
+  if constexpr (ALGO == 1) {
+    // the literal walk reads every width's tables; the leaf-parallel search
+    // builds them lazily for the widths that have a live call (search_v2)
+    for (int w = lane; w < nDG; w += 32)
+      build_width_tables<EXACT>(w / Gi + 1, w % Gi, Gi, sizes, c_start, c_list, o_key, o_dnt, o_tau, t_up, t_dn,
+                                t_tau);
   }
   if constexpr (ALGO == 1) { ring_done[lane] = 0; ring_done[lane + 32] = 0; }
   __syncwarp();
@@ -1274,7 +1321,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
                                        slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
                                        tot_v, tot_p,
                                        CountsMode{A.prm.exhaustive_counts != 0, c_start, c_list, o_key, o_dnt},
-                                       NI == 1 ? A.ctab : nullptr)) {
+                                       NI == 1 ? A.ctab : nullptr, sizes)) {
       // leaf counts overflow the u32 unranking tables: hand the instance to
       // the literal walk (second pass of launch_dftsp)
       put_status(EB_STATUS_FALLBACK, -1);
@@ -1497,7 +1544,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
 }
 
 template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI>
-__global__ void __launch_bounds__(128, 4) dftsp_kernel(DftspArgs A) {
+__global__ void __launch_bounds__(128, 4) dftsp_kernel(const __grid_constant__ DftspArgs A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   const int warp = threadIdx.x >> 5;
   unsigned char* smem = smem_all + warp * A.warp_bytes;
@@ -1523,7 +1570,7 @@ __global__ void __launch_bounds__(128, 4) dftsp_kernel(DftspArgs A) {
 // per block otherwise.  Instances come from an atomic counter; the narrow
 // ones were solved by the main pass.
 template <bool PRUNE, bool INCL, bool EXACT>
-__global__ void __launch_bounds__(32, 1) dftsp_wide_kernel(DftspArgs A, unsigned char* gscratch) {
+__global__ void __launch_bounds__(32, 1) dftsp_wide_kernel(const __grid_constant__ DftspArgs A, unsigned char* gscratch) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   unsigned char* smem = gscratch ? gscratch + (size_t)blockIdx.x * A.warp_bytes : smem_all;
   for (;;) {
@@ -1548,7 +1595,7 @@ template <bool PRUNE, bool INCL, bool EXACT, int NI>
 #ifndef EB_LOCK_MINB
 #define EB_LOCK_MINB 1
 #endif
-__global__ void __launch_bounds__(EB_LOCK_THREADS, EB_LOCK_MINB) dftsp_lock_kernel(DftspArgs A) {
+__global__ void __launch_bounds__(EB_LOCK_THREADS, EB_LOCK_MINB) dftsp_lock_kernel(const __grid_constant__ DftspArgs A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   __shared__ int s_base;
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1626,6 +1673,15 @@ __global__ void dfs_single_kernel(int z, int ncls, const int32_t* sizes, const i
 // Host-side launcher (device pointers, caller's stream).
 // ---------------------------------------------------------------------------
 size_t dftsp_warp_bytes(int K, int G, bool exact) { return make_lay(K, G, exact, true).total; }
+
+#ifdef EB_STATS
+extern "C" int eb_debug_stats(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_stats, sizeof(unsigned long long) * 16);
+  if (reset) { unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_stats, z, sizeof(z)); }
+  return 0;
+}
+#endif
 
 static int launch_one(eb_handle* h, cudaStream_t st, void (*kern)(DftspArgs), const DftspArgs& A, int warps,
                       size_t smem, int64_t n_inst) {
