@@ -344,7 +344,8 @@ def main():
         e2e = {"value": world * n * args.steps / wire_s, "unit": "instances/s", "h2d_bytes_per_step": int(wb.nbytes()),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": wire_s / args.steps * 1e3,
                "path": "eb_dftsp_batch_packed(EB_MEM_HOST): pinned host buffers in the compact wire format "
-                       "(id i32, tokens u16, uniform uplink power), chunks n/64 doubling to n/16 on a 3-stream pipeline",
+                       "(tokens u16, uniform uplink power, ids = row positions since they rise along every "
+                       "instance, uniform offsets), chunks n/64 doubling to n/16 on a 3-stream pipeline",
                "wide": {"value": world * n * args.steps / wide_s, "h2d_bytes_per_step": int(h2d_wide),
                         "ms_per_step": wide_s / args.steps * 1e3, "path": "eb_dftsp_batch(EB_MEM_HOST), eb_requests"}}
 

@@ -193,6 +193,11 @@ int32_t eb_dftsp_batch(eb_handle *h, const eb_context *ctxs, int32_t n_ctx,
  * (feasibility.py:36-37) are Python ints.  The caller checks they fit
  * (paper_2405_07140_b200/soa.py pack_wire does). */
 typedef struct eb_requests_packed {
+  /* NULL: ids are the request positions (row indices).  The search only
+   * compares ids within an instance (tie-breaks dftsp.py:78,257; the
+   * duplicate check; the solution's id order dftsp.py:281), so any
+   * increasing numbering of an instance's rows gives identical results;
+   * this is how Monte Carlo instances number their candidates. */
   const int32_t *id;
   const uint16_t *prompt_tokens;
   const uint16_t *output_tokens;
@@ -207,7 +212,7 @@ typedef struct eb_requests_packed {
 typedef struct eb_batch_packed {
   int64_t n_inst;
   int64_t n_req;              /* == offsets[n_inst] */
-  const int64_t *offsets;     /* n_inst + 1 */
+  const int64_t *offsets;     /* n_inst + 1, or NULL: every instance has k_max requests */
   const int32_t *ctx_index;   /* n_inst, or NULL = context 0 for all */
   eb_requests_packed req;
   int32_t k_max;              /* required: max offsets[i+1]-offsets[i] (<= EB_MAX_K) */

@@ -141,23 +141,29 @@ eb_requests upload_req(Stage& S, const eb_requests& r, int64_t lo, int64_t n) {
 
 // Wire format -> eb_requests columns (lossless widening; uniform uplink
 // power broadcast).  deadline/waiting/gain are already f64 and stay in place.
-__global__ void widen_wire_kernel(int64_t nr, const int32_t* __restrict__ id32,
+__global__ void widen_wire_kernel(int64_t nr, int64_t row0, const int32_t* __restrict__ id32,
                                   const uint16_t* __restrict__ p16, const uint16_t* __restrict__ o16,
                                   const double* __restrict__ pw, int uniform, int64_t* __restrict__ id64,
                                   int32_t* __restrict__ p32, int32_t* __restrict__ o32, double* __restrict__ pw64) {
   const double pw0 = uniform ? pw[0] : 0.0;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nr; j += (int64_t)gridDim.x * blockDim.x) {
-    id64[j] = id32[j];
+    id64[j] = id32 ? (int64_t)id32[j] : row0 + j;      // NULL: ids are row positions
     p32[j] = p16[j];
     o32[j] = o16[j];
     pw64[j] = uniform ? pw0 : pw[j];
   }
 }
 
+// Uniform instance sizes: offsets of instances [i0, i0 + ni] are i * k.
+__global__ void uniform_offsets_kernel(int64_t ni, int64_t i0, int k, int64_t* __restrict__ off) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= ni; i += (int64_t)gridDim.x * blockDim.x)
+    off[i] = (i0 + i) * k;
+}
+
 eb_requests upload_wire(Stage& S, const eb_requests_packed& r, int64_t lo, int64_t n) {
   eb_requests d;
   memset(&d, 0, sizeof(d));
-  const int32_t* id32 = S.up(r.id + lo, n);
+  const int32_t* id32 = r.id ? S.up(r.id + lo, n) : nullptr;
   const uint16_t* p16 = S.up(r.prompt_tokens + lo, n);
   const uint16_t* o16 = S.up(r.output_tokens + lo, n);
   d.deadline_s = S.up(r.deadline_s + lo, n);
@@ -172,7 +178,7 @@ eb_requests upload_wire(Stage& S, const eb_requests_packed& r, int64_t lo, int64
   int blocks = (int)((n + 255) / 256);
   if (blocks > 8 * S.h->num_sms) blocks = 8 * S.h->num_sms;
   if (blocks < 1) blocks = 1;
-  widen_wire_kernel<<<blocks, 256, 0, S.st>>>(n, id32, p16, o16, pw, r.uplink_power_uniform != 0, id64, p32,
+  widen_wire_kernel<<<blocks, 256, 0, S.st>>>(n, lo, id32, p16, o16, pw, r.uplink_power_uniform != 0, id64, p32,
                                                o32, pw64);
   ++S.h->launches;
   cudaError_t e = cudaGetLastError();
@@ -197,16 +203,30 @@ template <typename Upload>
 int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const eb_search_params& prm, int64_t n,
                         const int64_t* offsets, const int32_t* ctx_index, int K, int64_t n_wide,
                         const eb_dftsp_result& out, Upload upload) {
-  // Chunking: the first chunk's copy is exposed pipeline fill, so chunks
-  // start at n/64 and double up to n/16 (never below 8192 instances).
+  // offsets == NULL: every instance has K requests (wire format only)
+  auto off_at = [&](int64_t i) -> int64_t { return offsets ? offsets[i] : i * (int64_t)K; };
+  // Chunking: the first chunk's copy and the last chunk's search are the
+  // exposed pipeline fill and drain, so chunk sizes ramp n/64, n/32, n/16,
+  // ..., n/16, n/32, n/64 (never below 8192 instances).
   std::vector<int64_t> cut{0};
   {
     const int64_t full = (n + 15) / 16 > 8192 ? (n + 15) / 16 : 8192;
-    int64_t step = n / 64 > 8192 ? n / 64 : 8192;
-    while (cut.back() < n) {
-      cut.push_back(cut.back() + step < n ? cut.back() + step : n);
-      step = step * 2 < full ? step * 2 : full;
+    const int64_t small = n / 64 > 8192 ? n / 64 : 8192;
+    std::vector<int64_t> ramp;                       // n/64, n/32 (< full)
+    for (int64_t s = small; s < full; s *= 2) ramp.push_back(s);
+    int64_t head = 0;
+    for (int64_t s : ramp) head += s;
+    int64_t left = n;
+    for (int64_t s : ramp) { if (left <= 0) break; cut.push_back(cut.back() + (s < left ? s : left)); left -= s; }
+    // middle at `full`, keeping room for the mirrored ramp at the end
+    while (left > head + full) { cut.push_back(cut.back() + full); left -= full; }
+    if (left > head) { cut.push_back(cut.back() + (left - head)); left = head; }
+    for (auto it = ramp.rbegin(); it != ramp.rend() && left > 0; ++it) {
+      const int64_t s = *it < left ? *it : left;
+      cut.push_back(cut.back() + s);
+      left -= s;
     }
+    if (cut.back() < n) cut.push_back(n);
   }
   const int nchunks = (int)cut.size() - 1;
   // The pipeline streams fork from / join back into the handle's stream so
@@ -223,8 +243,22 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
     stages.push_back(S);
     if (!d_ctx[c % 3]) d_ctx[c % 3] = S->up(ctxs, (size_t)n_ctx);
     const int64_t i0 = cut[c], i1 = cut[c + 1], ni = i1 - i0;
-    const int64_t R0 = offsets[i0], R1 = offsets[i1], nr = R1 - R0;
-    const int64_t* d_off = S->up(offsets + i0, (size_t)ni + 1);
+    const int64_t R0 = off_at(i0), R1 = off_at(i1), nr = R1 - R0;
+    const int64_t* d_off;
+    if (offsets) {
+      d_off = S->up(offsets + i0, (size_t)ni + 1);
+    } else {
+      int64_t* o = S->alloc<int64_t>((size_t)ni + 1);
+      if (o) {
+        int blocks = (int)((ni + 256) / 256);
+        if (blocks > 4 * h->num_sms) blocks = 4 * h->num_sms;
+        uniform_offsets_kernel<<<blocks, 256, 0, st>>>(ni, i0, K, o);
+        ++h->launches;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) S->err = cuda_fail(e, "uniform_offsets_kernel");
+      }
+      d_off = o;
+    }
     const int32_t* d_ci = ctx_index ? S->up(ctx_index + i0, (size_t)ni) : nullptr;
     eb_requests d_req = upload(*S, R0, nr);
     eb_dftsp_result d_out;
@@ -430,16 +464,17 @@ int32_t eb_dftsp_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, cons
 int32_t eb_dftsp_batch_packed(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_search_params* prm,
                               const eb_batch_packed* b, eb_dftsp_result* out, int32_t mem) {
   if (!h || !ctxs || n_ctx < 1 || !prm || !b || !out || !out->status || !out->z_found ||
-      !out->nodes_visited || !out->nodes_pruned || b->n_inst < 0 || !b->offsets)
+      !out->nodes_visited || !out->nodes_pruned || b->n_inst < 0)
     return EB_ERR_INVALID_ARG;
   if (prm->ladder_len < 0 || prm->ladder_len > EB_MAX_CLASSES) return EB_ERR_INVALID_ARG;
   const eb_requests_packed& r = b->req;
-  if (!r.id || !r.prompt_tokens || !r.output_tokens || !r.deadline_s || !r.waiting_s || !r.channel_gain ||
+  if (!r.prompt_tokens || !r.output_tokens || !r.deadline_s || !r.waiting_s || !r.channel_gain ||
       !r.uplink_power_w)
     return EB_ERR_INVALID_ARG;
   if (prm->collect_trajectory && (!out->traj || !out->traj_offsets)) return EB_ERR_INVALID_ARG;
   if (mem != EB_MEM_HOST) return EB_ERR_INVALID_ARG;
   if (b->k_max < 1 || b->k_max > EB_MAX_K) return EB_ERR_INVALID_ARG;
+  if (!b->offsets && b->n_req != b->n_inst * (int64_t)b->k_max) return EB_ERR_INVALID_ARG;
   EB_CUDA(cudaSetDevice(h->device));
   if (b->n_inst == 0) return EB_OK;
   return dftsp_host_pipeline(h, ctxs, n_ctx, *prm, b->n_inst, b->offsets, b->ctx_index, b->k_max, 0, *out,

@@ -201,7 +201,7 @@ def solve_batch(batch: InstanceBatch | WireBatch, *, pruning=True, inclusive_bou
     ``algorithm``: 0 auto, 1 literal node walk (one dfs call per lane), 2
     leaf-parallel with combinatorial node counts -- identical results."""
     n, nr = batch.n_inst, batch.n_req
-    sizes = np.diff(batch.offsets)
+    sizes = batch.sizes() if isinstance(batch, WireBatch) else np.diff(batch.offsets)
     res = BatchResult(status=np.zeros(n, np.int32), error_index=np.full(n, -1, np.int32),
                       z_found=np.zeros(n, np.int32), nodes_visited=np.zeros(n, np.int64),
                       nodes_pruned=np.zeros(n, np.int64), n_classes=np.zeros(n, np.int32),

@@ -146,18 +146,24 @@ WIRE_FIELDS = (("id", np.int32), ("prompt_tokens", np.uint16), ("output_tokens",
 
 @dataclass
 class WireBatch:
-    """An InstanceBatch in the compact wire format (host arrays only)."""
+    """An InstanceBatch in the compact wire format (host arrays only).
 
-    offsets: np.ndarray
+    ``offsets`` None: every instance has ``k_max`` requests.  ``columns['id']``
+    None: ids are the request positions (valid when each instance's ids
+    increase along its rows: the search only compares ids within an
+    instance, so the results are identical)."""
+
+    offsets: np.ndarray | None
     columns: dict
     uplink_power_w: np.ndarray      # one value (uniform) or one per request
     contexts: np.ndarray
     ctx_index: object = None
     k_max: int = 0
+    n_inst_: int = 0
 
     @property
     def n_inst(self) -> int:
-        return int(self.offsets.shape[0]) - 1
+        return int(self.offsets.shape[0]) - 1 if self.offsets is not None else self.n_inst_
 
     @property
     def n_req(self) -> int:
@@ -167,10 +173,16 @@ class WireBatch:
     def uniform_power(self) -> bool:
         return self.uplink_power_w.shape[0] == 1
 
+    def sizes(self) -> np.ndarray:
+        if self.offsets is None:
+            return np.full(self.n_inst, self.k_max, np.int64)
+        return np.diff(self.offsets)
+
     def nbytes(self) -> int:
         """Bytes one host->device pass of this batch moves."""
-        n = sum(int(a.nbytes) for a in self.columns.values()) + int(self.uplink_power_w.nbytes)
-        n += int(self.offsets.nbytes)
+        n = sum(int(a.nbytes) for a in self.columns.values() if a is not None) + int(self.uplink_power_w.nbytes)
+        if self.offsets is not None:
+            n += int(self.offsets.nbytes)
         if self.ctx_index is not None:
             n += int(self.ctx_index.nbytes)
         return n
@@ -178,13 +190,14 @@ class WireBatch:
     def struct(self) -> "_lib.eb_batch_packed":
         r = _lib.eb_requests_packed()
         for name, _ in WIRE_FIELDS:
-            setattr(r, name, ptr(self.columns[name]))
+            a = self.columns.get(name)
+            setattr(r, name, ptr(a) if a is not None else None)
         r.uplink_power_w = ptr(self.uplink_power_w)
         r.uplink_power_uniform = int(self.uniform_power)
         b = _lib.eb_batch_packed()
         b.n_inst = self.n_inst
         b.n_req = self.n_req
-        b.offsets = ptr(self.offsets)
+        b.offsets = ptr(self.offsets) if self.offsets is not None else None
         b.ctx_index = ptr(self.ctx_index)
         b.req = r
         b.k_max = int(self.k_max)
@@ -192,33 +205,50 @@ class WireBatch:
         return b
 
 
-def pack_wire(batch: InstanceBatch, pin=None) -> WireBatch | None:
+def pack_wire(batch: InstanceBatch, pin=None, implicit=True) -> WireBatch | None:
     """The wire-format copy of a host batch, or None when a column does not
     narrow losslessly (ids outside int32, token counts outside uint16) or an
-    instance is wider than EB_MAX_K.  ``pin`` (e.g. ``lambda a:
-    torch.from_numpy(a).pin_memory().numpy()``) places the arrays in pinned
-    memory."""
+    instance is wider than EB_MAX_K.  With ``implicit``, ids that increase
+    along every instance's rows and uniform instance sizes are not shipped.
+    ``pin`` (e.g. ``lambda a: torch.from_numpy(a).pin_memory().numpy()``)
+    places the arrays in pinned memory."""
     cols = batch.columns
-    if batch.n_inst and int(np.diff(batch.offsets).max()) > _lib.EB_MAX_K:
+    sizes = np.diff(batch.offsets)
+    if batch.n_inst and int(sizes.max()) > _lib.EB_MAX_K:
         return None
     ids, pt, ot = cols["id"], cols["prompt_tokens"], cols["output_tokens"]
-    if ids.size and (ids.min() < -2**31 or ids.max() > INT32_MAX):
-        return None
     for a in (pt, ot):
         if a.size and (a.min() < 0 or a.max() > 0xFFFF):
             return None
-    out = {name: np.ascontiguousarray(cols[name], dtype=dt) for name, dt in WIRE_FIELDS}
+    out = {name: np.ascontiguousarray(cols[name], dtype=dt) for name, dt in WIRE_FIELDS if name != "id"}
+    rising = False
+    if implicit and ids.size:
+        step = np.diff(ids) > 0
+        first = batch.offsets[1:-1]                   # rows that start an instance (not compared)
+        first = first[(first > 0) & (first < ids.size)]
+        step[first - 1] = True
+        rising = bool(step.all())
+    if rising:
+        out["id"] = None
+    else:
+        if ids.size and (ids.min() < -2**31 or ids.max() > INT32_MAX):
+            return None
+        out["id"] = np.ascontiguousarray(ids, dtype=np.int32)
     pw = np.ascontiguousarray(cols["uplink_power_w"], dtype=np.float64)
     if pw.size and (pw.view(np.int64) == pw[:1].view(np.int64)).all():    # same bits: uniform
         pw = pw[:1].copy()
+    k = int(batch.k_max) if batch.k_max else (int(sizes.max()) if batch.n_inst else 1)
+    k = max(1, k)
     off = np.ascontiguousarray(batch.offsets, dtype=np.int64)
+    if implicit and batch.n_inst and (sizes == k).all():
+        off = None
     ci = None if batch.ctx_index is None else np.ascontiguousarray(batch.ctx_index, dtype=np.int32)
     if pin is not None:
-        out = {k: pin(v) for k, v in out.items()}
-        pw, off = pin(pw), pin(off)
+        out = {kk: (pin(v) if v is not None else None) for kk, v in out.items()}
+        pw = pin(pw)
+        off = None if off is None else pin(off)
         ci = None if ci is None else pin(ci)
-    k = int(batch.k_max) if batch.k_max else (int(np.diff(off).max()) if batch.n_inst else 1)
-    return WireBatch(off, out, pw, batch.contexts, ci, max(1, k))
+    return WireBatch(off, out, pw, batch.contexts, ci, k, batch.n_inst)
 
 
 def search_params(pruning=True, inclusive_bound=False, exact_tau=False, collect_trajectory=False, ladder=None,

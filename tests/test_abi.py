@@ -89,6 +89,8 @@ def test_pack_wire_is_lossless_or_refuses():
     batch, _ = random_batch(5, 200)
     w = pack_wire(batch)
     assert w is not None and w.uniform_power
+    assert w.columns["id"] is not None          # random ids do not rise along the rows: shipped
+    assert w.offsets is not None                # ragged sizes: shipped
     for name in ("id", "prompt_tokens", "output_tokens"):
         assert np.array_equal(w.columns[name].astype(np.int64), batch.columns[name].astype(np.int64))
     for name in ("deadline_s", "waiting_s", "channel_gain"):
@@ -105,6 +107,28 @@ def test_pack_wire_is_lossless_or_refuses():
         c3[name] = c3[name].copy()
         c3[name][0] = bad
         assert pack_wire(type(batch)(batch.offsets, c3, batch.contexts, batch.ctx_index, batch.k_max)) is None
+
+
+def test_pack_wire_implicit_ids_and_offsets():
+    """Ids rising along each instance's rows and uniform sizes are not shipped
+    (positions reproduce every id comparison); anything else is."""
+    import numpy as np
+    from paper_2405_07140_b200.soa import InstanceBatch, pack_wire
+    from gen_random import random_batch
+    batch, _ = random_batch(6, 50, k_min=7, k_max=7)
+    cols = dict(batch.columns)
+    ids = np.concatenate([np.sort(cols["id"][batch.offsets[i]:batch.offsets[i + 1]]) for i in range(batch.n_inst)])
+    cols["id"] = ids
+    b = InstanceBatch(batch.offsets, cols, batch.contexts, batch.ctx_index, 7)
+    w = pack_wire(b)
+    assert w.columns["id"] is None and w.offsets is None and w.n_inst == 50 and w.k_max == 7
+    assert np.array_equal(w.sizes(), np.full(50, 7))
+    full = pack_wire(b, implicit=False)
+    assert w.nbytes() == full.nbytes() - 4 * b.n_req - 8 * (b.n_inst + 1)
+    cols2 = dict(cols)
+    cols2["id"] = ids.copy()
+    cols2["id"][3], cols2["id"][4] = ids[4], ids[3]          # one descent inside instance 0
+    assert pack_wire(InstanceBatch(batch.offsets, cols2, batch.contexts, batch.ctx_index, 7)).columns["id"] is not None
 
 
 def test_no_gpu_means_loud_failure():

@@ -235,3 +235,21 @@ def test_gpu_wire_format_matches_wide_call(uniform):
             assert np.array_equal(getattr(dev, k), getattr(wire, k)), (lad, k)
         orc = oracle.dftsp_batch(sb, ladder=lad, threads=8)
         _assert_same(wire, orc, sb, f"wire ladder {lad}")
+
+
+def test_gpu_wire_format_implicit_ids_and_offsets():
+    """Row-position ids and implicit uniform offsets (eb_dftsp_batch_packed with
+    id = NULL, offsets = NULL) give exactly the wide call's results when the
+    ids rise along each instance's rows."""
+    from paper_2405_07140_b200 import synth
+    from paper_2405_07140_b200.soa import pack_wire
+    b = synth.generate(synth.CONFIG2, 20000, seed=99)           # ids 0..K-1 per instance
+    w = pack_wire(b)
+    assert w.columns["id"] is None and w.offsets is None
+    lad = (128, 256, 512)
+    dev = search.solve_batch(b, ladder=lad)
+    wire = search.solve_batch(w, ladder=lad)
+    for k in RES_KEYS + ("solution", "metrics", "error_index"):
+        assert np.array_equal(getattr(dev, k), getattr(wire, k)), k
+    orc = oracle.dftsp_batch(b, ladder=lad, threads=8)
+    _assert_same(wire, orc, b, "wire implicit")
