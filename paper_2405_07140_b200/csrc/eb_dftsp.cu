@@ -564,7 +564,39 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
   found = false;
   const int total_calls = n * (n + 1) / 2;
   EB_STAT(0, 1);
-  for (int c0 = 0; c0 < total_calls && !found; c0 += 32) {
+  // Whole targets z first: the greedy leaf of the widest pool (d = n) has the
+  // least memory and latency of any width's greedy leaf (more short requests
+  // to choose from), and every width d >= z has a cap no larger than width
+  // z's (tau descends with d).  If it fails width z's caps by the margin, no
+  // call (z, d) can contain a passing leaf, so the call sequence starts at
+  // the largest z that survives (lanes = z).  Counts mode needs every call.
+  int c_first = 0;
+  if (!cm.on) {
+    const LevelInfo* rown = lvl + (size_t)(n - 1) * Gi;
+    const int mn = ncls_d[n - 1];
+    int zhi = 0;
+    for (int z = lane + 1; z <= n; z += 32) {
+      const double k3z = mul(k3, i2d(z));
+      const double slot_cap = has_cap ? sub(slot_base, k3z) : INF;
+      const double mem_cap = sub(k2, i2d((int64_t)padded * z));
+      int rem = z;
+      int64_t mem = 0;
+      double lat = 0.0;
+      for (int k = 0; k < mn && rem > 0; ++k) {
+        const LevelInfo li = rown[k];
+        const int cc = min(rem, (int)li.size);
+        mem += (int64_t)cc * c_len[li.g];
+        lat = add(lat, mul(i2d(cc), c_w[li.g]));
+        rem -= cc;
+      }
+      const double lat_cap = EXACT ? slot_cap : pymin(sub(o_tau[z - 1], k3z), slot_cap);
+      if (!(fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap)))
+        zhi = z;
+    }
+    zhi = __reduce_max_sync(EB_FULL, zhi);
+    c_first = zhi > 0 ? (n - zhi) * (n - zhi + 1) / 2 : total_calls;
+  }
+  for (int c0 = c_first; c0 < total_calls && !found; c0 += 32) {
     const int c = c0 + lane;
     int z = 0, d = 0;
     bool live = false;
