@@ -90,11 +90,22 @@ struct Stage {
   cudaStream_t st;
   std::vector<void*> bufs;
   int err = EB_OK;
+  unsigned char* arena = nullptr;   // optional bump arena (no allocation calls per buffer)
+  size_t cap = 0, used = 0;
   Stage(eb_handle* hh, cudaStream_t s) : h(hh), st(s) {}
+  Stage(eb_handle* hh, cudaStream_t s, void* a, size_t bytes) : h(hh), st(s), arena((unsigned char*)a), cap(bytes) {}
   ~Stage() { for (void* p : bufs) cudaFreeAsync(p, st); }
   template <typename T>
   T* alloc(size_t count) {
     if (count == 0) count = 1;
+    if (arena) {
+      const size_t b = (count * sizeof(T) + 255) & ~(size_t)255;
+      if (used + b <= cap) {
+        T* q = (T*)(arena + used);
+        used += b;
+        return q;
+      }
+    }
     void* p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, count * sizeof(T), st);
     if (e != cudaSuccess) { err = cuda_fail(e, "cudaMallocAsync"); return nullptr; }
@@ -207,11 +218,13 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
   auto off_at = [&](int64_t i) -> int64_t { return offsets ? offsets[i] : i * (int64_t)K; };
   // Chunking: the first chunk's copy and the last chunk's search are the
   // exposed pipeline fill and drain, so chunk sizes ramp n/64, n/32, n/16,
-  // ..., n/16, n/32, n/64 (never below 8192 instances).
+  // ..., n/16, n/32, n/64.  Every chunk costs ~15 dependent copies and
+  // launches (~0.2 ms of latency, measured by tools/host_overhead.py), so
+  // chunks never go below 16384 instances (32768 in the middle).
   std::vector<int64_t> cut{0};
   {
-    const int64_t full = (n + 15) / 16 > 8192 ? (n + 15) / 16 : 8192;
-    const int64_t small = n / 64 > 8192 ? n / 64 : 8192;
+    const int64_t full = (n + 15) / 16 > 32768 ? (n + 15) / 16 : 32768;
+    const int64_t small = n / 64 > 16384 ? n / 64 : 16384;
     std::vector<int64_t> ramp;                       // n/64, n/32 (< full)
     for (int64_t s = small; s < full; s *= 2) ramp.push_back(s);
     int64_t head = 0;
@@ -236,12 +249,44 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
   // context table once per pipe stream (tiny)
   std::vector<Stage*> stages;
   int rc = EB_OK;
-  eb_context* d_ctx[3] = {nullptr, nullptr, nullptr};
+  // the context table once, through the pinned staging buffer (a pageable
+  // copy would block the host), on pipe 0; the other pipes wait for it
+  eb_context* d_ctx = nullptr;
+  {
+    const size_t cb = sizeof(eb_context) * (size_t)n_ctx;
+    int e = ensure_pinned(h, cb);
+    if (e) return e;
+    memcpy(h->pinned, ctxs, cb);
+    Stage* S0 = new Stage(h, h->pipe[0]);
+    stages.push_back(S0);
+    d_ctx = S0->up((const eb_context*)h->pinned, (size_t)n_ctx);
+    if (S0->err) { rc = S0->err; }
+    EB_CUDA(cudaEventRecord(h->ev[1], h->pipe[0]));
+    EB_CUDA(cudaStreamWaitEvent(h->pipe[1], h->ev[1], 0));
+    EB_CUDA(cudaStreamWaitEvent(h->pipe[2], h->ev[1], 0));
+  }
+  // one arena per pipeline stream, sized for its largest chunk: per instance
+  // offsets, context index and outputs; per request the staged and widened
+  // columns and the solution; per trajectory row 32 B; 256 B alignment slack
+  // per buffer
+  for (int c = 0; c < nchunks && rc == EB_OK; ++c) {
+    const int64_t i0 = cut[c], i1 = cut[c + 1];
+    size_t bytes = 48 * 256 + (size_t)(i1 - i0 + 1) * 320 + (size_t)(off_at(i1) - off_at(i0)) * 96;
+    if (prm.collect_trajectory) bytes += (size_t)(out.traj_offsets[i1] - out.traj_offsets[i0]) * 32;
+    const int sidx = c % 3;
+    if (h->arena_bytes[sidx] < bytes) {
+      if (h->arena[sidx]) cudaFreeAsync(h->arena[sidx], h->pipe[sidx]);
+      h->arena[sidx] = nullptr;
+      h->arena_bytes[sidx] = 0;
+      cudaError_t e = cudaMallocAsync(&h->arena[sidx], bytes, h->pipe[sidx]);
+      if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMallocAsync(arena)"); break; }
+      h->arena_bytes[sidx] = bytes;
+    }
+  }
   for (int c = 0; c < nchunks && rc == EB_OK; ++c) {
     cudaStream_t st = h->pipe[c % 3];
-    Stage* S = new Stage(h, st);
+    Stage* S = new Stage(h, st, h->arena[c % 3], h->arena_bytes[c % 3]);
     stages.push_back(S);
-    if (!d_ctx[c % 3]) d_ctx[c % 3] = S->up(ctxs, (size_t)n_ctx);
     const int64_t i0 = cut[c], i1 = cut[c + 1], ni = i1 - i0;
     const int64_t R0 = off_at(i0), R1 = off_at(i1), nr = R1 - R0;
     const int64_t* d_off;
@@ -283,7 +328,7 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
     }
     int* d_counter = S->alloc<int>(2);
     if (S->err) { rc = S->err; break; }
-    rc = launch_dftsp(h, st, d_ctx[c % 3], n_ctx, prm, ni, d_off, d_ci, R0, d_req, K, d_out, T0, d_counter, n_wide);
+    rc = launch_dftsp(h, st, d_ctx, n_ctx, prm, ni, d_off, d_ci, R0, d_req, K, d_out, T0, d_counter, n_wide);
     if (rc) break;
     S->down(out.status + i0, d_out.status, ni);
     S->down(out.error_index ? out.error_index + i0 : nullptr, d_out.error_index, ni);
@@ -391,8 +436,10 @@ int32_t eb_handle_destroy(eb_handle* h) {
   for (int i = 0; i < 3; ++i) { cudaStreamDestroy(h->pipe[i]); cudaEventDestroy(h->ev[i]); }
   if (h->dscratch) cudaFree(h->dscratch);
   if (h->pinned) cudaFreeHost(h->pinned);
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 3; ++i) {
     if (h->ctab[i]) cudaFree(h->ctab[i]);
+    if (h->arena[i]) cudaFree(h->arena[i]);
+  }
   delete h;
   return EB_OK;
 }

@@ -1717,9 +1717,34 @@ extern "C" int eb_debug_stats(unsigned long long* out, int reset) {
 
 static int launch_one(eb_handle* h, cudaStream_t st, void (*kern)(DftspArgs), const DftspArgs& A, int warps,
                       size_t smem, int64_t n_inst) {
-  EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));
+  // occupancy per (kernel, block, smem) and the largest dynamic shared
+  // memory attribute set per kernel, cached per thread (the host pipeline
+  // launches every kernel once per chunk).  The attribute is a maximum, so
+  // it is only ever raised.
+  struct Occ { void (*k)(DftspArgs); int warps; size_t smem; int per_sm; int dev; };
+  struct Attr { void (*k)(DftspArgs); size_t smem; int dev; };
+  static thread_local Occ occ[16];
+  static thread_local Attr attr[16];
+  static thread_local int nocc = 0, nattr = 0;
+  int ai = -1;
+  for (int i = 0; i < nattr && i < 16; ++i)
+    if (attr[i].k == kern && attr[i].dev == h->device) { ai = i; break; }
+  if (ai < 0 || attr[ai].smem < smem) {
+    EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (ai < 0) { ai = nattr % 16; ++nattr; }
+    attr[ai] = Attr{kern, smem, h->device};
+  }
+  int per_sm = -1;
+  for (int i = 0; i < nocc && i < 16; ++i)
+    if (occ[i].k == kern && occ[i].warps == warps && occ[i].smem == smem && occ[i].dev == h->device) {
+      per_sm = occ[i].per_sm;
+      break;
+    }
+  if (per_sm < 0) {
+    EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));
+    occ[nocc % 16] = Occ{kern, warps, smem, per_sm, h->device};
+    ++nocc;
+  }
   if (per_sm < 1) per_sm = 1;
   int64_t want = (n_inst + warps - 1) / warps;
   int64_t grid = (int64_t)per_sm * h->num_sms;

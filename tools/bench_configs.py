@@ -12,6 +12,10 @@
            rank over NCCL), z cross-checked against DFTSP (optimality)
   config5  tight-memory OPT-13B edge (5 output classes): DFTSP instances/s
 
+kernel_inst_per_s: inputs resident in HBM (eb_dftsp_batch, EB_MEM_DEVICE);
+wire_e2e_inst_per_s: pinned host buffers through eb_dftsp_batch_packed (copies
+included); api_inst_per_s: search.solve_batch on pageable numpy arrays (the
+Python convenience API, allocation and pageable copies included).
 CPU columns time the C oracle port on a bounded sample with all host threads.
 """
 from __future__ import annotations
@@ -42,6 +46,63 @@ def ev_time(fn, reps=3):
         torch.cuda.synchronize()
         t.append(time.perf_counter() - t0)
     return min(t)
+
+
+def device_rates(batch, ladder, reps=3):
+    """(kernel inst/s with inputs resident in HBM, end-to-end inst/s through
+    eb_dftsp_batch_packed with pinned host buffers) -- bench.py's two legs."""
+    import ctypes
+    import torch
+    from paper_2405_07140_b200.soa import pack_wire, search_params
+    dev = torch.device("cuda", 0)
+    h = _lib.handle(0)
+    st = torch.cuda.Stream()
+    h.set_stream(st.cuda_stream)
+    n, nr = batch.n_inst, batch.n_req
+
+    def td(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    used = [k for k in batch.columns if k != "tolerance"]
+    db = InstanceBatch(td(batch.offsets), {k: td(batch.columns[k]) for k in used}, batch.contexts,
+                       td(batch.ctx_index), batch.k_max, on_device=True).struct()
+    d_ctx = td(batch.contexts.view(np.uint8))
+    outs = {"status": (n, torch.int32), "z_found": (n, torch.int32), "nodes_visited": (n, torch.int64),
+            "nodes_pruned": (n, torch.int64), "solution": (nr, torch.int32)}
+    dres, hres = _lib.eb_dftsp_result(), _lib.eb_dftsp_result()
+    keep = []
+    for k, (m, dt) in outs.items():
+        a = torch.zeros(m, dtype=dt, device=dev)
+        b = torch.zeros(m, dtype=dt).pin_memory()
+        keep += [a, b]
+        setattr(dres, k, a.data_ptr())
+        setattr(hres, k, b.data_ptr())
+    prm = search_params(ladder=ladder)
+    ref = lambda x: ctypes.cast(ctypes.pointer(x), ctypes.c_void_p)  # noqa: E731
+    wb = pack_wire(batch, pin=lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy())
+    wbs = wb.struct()
+
+    def k_dev():
+        _lib.check(h.lib.eb_dftsp_batch(h.ptr, d_ctx.data_ptr(), len(batch.contexts), ref(prm), ref(db), ref(dres),
+                                        _lib.EB_MEM_DEVICE), "device")
+
+    def k_wire():
+        _lib.check(h.lib.eb_dftsp_batch_packed(h.ptr, batch.contexts.ctypes.data, len(batch.contexts), ref(prm),
+                                               ref(wbs), ref(hres), _lib.EB_MEM_HOST), "wire")
+
+    def timed(fn):
+        with torch.cuda.stream(st):
+            fn()
+            st.synchronize()
+            best = float("inf")
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                fn()
+                e1.record(st)
+                e1.synchronize()
+                best = min(best, e0.elapsed_time(e1) / 1e3)
+        return n / best
+    return timed(k_dev), timed(k_wire)
 
 
 def cpu_rate(batch, ladder, sample, threads):
@@ -89,10 +150,12 @@ def config3(threads, n_per_k):
             b = synth.generate(w, n, seed=2405_0714 + K)
             dt = ev_time(lambda: search.solve_batch(b, ladder=(128, 256, 512)), reps=2)
             res = search.solve_batch(b, ladder=(128, 256, 512))
+            kr, er = device_rates(b, (128, 256, 512))
             cr, orc = cpu_rate(b, (128, 256, 512), 2000 if K <= 25 else 300, threads)
             ok = bool(np.array_equal(orc["nodes_visited"], res.nodes_visited[:len(orc["nodes_visited"])]))
             out.append({"K": K, "deadline_scale": ds, "tolerance_cap": tc, "instances": n,
-                        "dftsp_e2e_inst_per_s": round(n / dt, 1), "mean_z": float(res.z_found.mean()),
+                        "kernel_inst_per_s": round(kr, 1), "wire_e2e_inst_per_s": round(er, 1),
+                        "api_inst_per_s": round(n / dt, 1), "mean_z": float(res.z_found.mean()),
                         "mean_nodes_visited": float(res.nodes_visited.mean()), "cpu_port_inst_per_s": round(cr, 1),
                         "parity_sample_ok": ok})
     return {"config": "config3: K sweep x deadline x tolerance (w8a16)", "rows": out}
@@ -125,9 +188,11 @@ def config5(threads, n):
     lad = synth.CONFIG5.outputs
     dt = ev_time(lambda: search.solve_batch(b, ladder=lad), reps=2)
     res = search.solve_batch(b, ladder=lad)
+    kr, er = device_rates(b, lad)
     cr, orc = cpu_rate(b, lad, 3000, threads)
     ok = bool(np.array_equal(orc["nodes_visited"], res.nodes_visited[:len(orc["nodes_visited"])]))
-    return {"config": synth.CONFIG5.name, "instances": n, "dftsp_e2e_inst_per_s": round(n / dt, 1),
+    return {"config": synth.CONFIG5.name, "instances": n, "kernel_inst_per_s": round(kr, 1),
+            "wire_e2e_inst_per_s": round(er, 1), "api_inst_per_s": round(n / dt, 1),
             "mean_z": float(res.z_found.mean()), "mean_nodes_visited": float(res.nodes_visited.mean()),
             "cpu_port_inst_per_s": round(cr, 1), "cpu_threads": threads, "parity_sample_ok": ok}
 
