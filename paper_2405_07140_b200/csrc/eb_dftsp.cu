@@ -107,7 +107,7 @@ struct DftspArgs {
   eb_dftsp_result out;        // per-instance arrays launch-local; solution at row - req_base
   int64_t traj_base;          // absolute row of out.traj element 0
   int* counter;               // [0] instance queue, [1] fallback count
-  const uint2* ctab;          // node-count table for this flag variant (K <= 32), or null
+  const uint2* ctab;          // node-count table for this flag variant (K <= 64), or null
   Lay lay;                    // per-warp shared-memory layout (make_lay(K, G, exact, algorithm 2))
   int fallback_pass;
 };
@@ -441,35 +441,47 @@ __device__ __forceinline__ void last_level_prefix(uint32_t s, uint32_t rr, uint6
   }
 }
 
-// Node-count tables for instances of at most 32 requests and at most three
-// output classes.  Per partition shape (m classes of sizes s0, s1, s2, in
-// level order) they hold PF0(q) = sum over r = 1..q of F(0, r) (visited,
-// pruned), the full-traversal counts of dfs calls with target r computed by
-// the same recurrence as search_v2 (level_counts_f / last_level_prefix).
-// Summing F(0, z) over a z range is then two lookups.  Layout (uint2
-// entries): m = 3 at [s0][s1][s2][q], m = 2 at CT^4 + [s0][s1][q], m = 1 at
-// CT^4 + CT^3 + [s0][q].
-constexpr int CT = 33;
-constexpr size_t CT_ENTRIES = (size_t)CT * CT * CT * CT + (size_t)CT * CT * CT + (size_t)CT * CT;
+// Node-count tables for instances of at most 64 requests and at most three
+// output classes.  Per partition shape (m classes of sizes s0, s1, s2 >= 1,
+// in level order, s0 + s1 + s2 <= 64) a row holds PF0(q) = sum over
+// r = 1..q of F(0, r) (visited, pruned), q = 0..64: the full-traversal counts
+// of dfs calls with target r, computed by the same recurrence as search_v2
+// (level_counts_f / last_level_prefix).  Summing F(0, z) over a z range is
+// then two lookups.  Layout: a u32 header of row offsets -- O3[s0 * CT + s1]
+// = row of (s0, s1, 1), O2[s0] = row of (s0, 1), R1 = row of (1) -- then the
+// rows of CT uint2 entries (43,744 rows, 22.7 MB per flag variant).
+constexpr int CT = 65;
+constexpr int CT_HDR = CT * CT + CT + 1;                  // u32 entries
+constexpr size_t CT_HDR_BYTES = ((size_t)CT_HDR * 4 + 255) & ~(size_t)255;
+constexpr int CT_ROWS = 41664 + 2016 + 64;                // C(64,3) + C(64,2) + 64
 
-__host__ __device__ __forceinline__ size_t ct_base(int m, int s0, int s1, int s2) {
-  const size_t c3 = (size_t)CT * CT * CT * CT, c2 = (size_t)CT * CT * CT;
-  if (m == 3) return (((size_t)s0 * CT + s1) * CT + s2) * CT;
-  if (m == 2) return c3 + ((size_t)s0 * CT + s1) * CT;
-  return c3 + c2 + (size_t)s0 * CT;
+__host__ __device__ __forceinline__ int ct_row(const uint32_t* hdr, int m, int s0, int s1, int s2) {
+  if (m == 3) return (int)hdr[s0 * CT + s1] + s2 - 1;
+  if (m == 2) return (int)hdr[CT * CT + s0] + s1 - 1;
+  return (int)hdr[CT * CT + CT] + s0 - 1;
+}
+
+// Host: the header (row offsets in shape order).
+static void ct_header(uint32_t* hdr) {
+  for (int i = 0; i < CT_HDR; ++i) hdr[i] = 0;
+  uint32_t row = 0;
+  for (int s0 = 1; s0 <= 62; ++s0)
+    for (int s1 = 1; s0 + s1 <= 63; ++s1) { hdr[s0 * CT + s1] = row; row += 64 - s0 - s1; }
+  for (int s0 = 1; s0 <= 63; ++s0) { hdr[CT * CT + s0] = row; row += 64 - s0; }
+  hdr[CT * CT + CT] = row;
 }
 
 template <bool PRUNE, bool INCL>
-__global__ void count_table_kernel(uint2* T) {
+__global__ void count_table_kernel(const uint32_t* __restrict__ hdr, uint2* __restrict__ rows) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int n3 = 32 * 32 * 32, n2 = 32 * 32;
+  const int n3 = 64 * 64 * 64, n2 = 64 * 64;
   int m, sz[3] = {0, 0, 0};
-  if (t < n3) { m = 3; sz[0] = 1 + t / 1024; sz[1] = 1 + (t / 32) % 32; sz[2] = 1 + t % 32; }
-  else if (t < n3 + n2) { m = 2; sz[0] = 1 + (t - n3) / 32; sz[1] = 1 + (t - n3) % 32; }
-  else if (t < n3 + n2 + 32) { m = 1; sz[0] = 1 + (t - n3 - n2); }
+  if (t < n3) { m = 3; sz[0] = 1 + t / 4096; sz[1] = 1 + (t / 64) % 64; sz[2] = 1 + t % 64; }
+  else if (t < n3 + n2) { m = 2; sz[0] = 1 + (t - n3) / 64; sz[1] = 1 + (t - n3) % 64; }
+  else if (t < n3 + n2 + 64) { m = 1; sz[0] = 1 + (t - n3 - n2); }
   else return;
   const int d = sz[0] + sz[1] + sz[2];
-  if (d > 32) return;
+  if (d > 64) return;
   LevelInfo row[3];
   int tail = 0;
   for (int k = m - 1; k >= 0; --k) {
@@ -479,11 +491,10 @@ __global__ void count_table_kernel(uint2* T) {
   }
   const uint32_t sl = sz[m - 1];
   auto pf_last = [&](int q, uint64_t& v, uint64_t& p) { last_level_prefix<PRUNE, INCL>(sl, (uint32_t)q, v, p); };
-  uint32_t RV[CT], RP[CT];
+  uint32_t RV[CT] = {}, RP[CT] = {};
   auto pf_row = [&](int q, uint64_t& v, uint64_t& p) { v = RV[q]; p = RP[q]; };
   if (m == 3) {                       // level 1 against the closed-form level 2, prefix-summed
     uint64_t av = 0, ap = 0;
-    RV[0] = RP[0] = 0;
     for (int r = 1; r <= d; ++r) {
       uint64_t fv, fp;
       level_counts_f<PRUNE, INCL>(row[1], false, r, pf_last, fv, fp);
@@ -491,10 +502,10 @@ __global__ void count_table_kernel(uint2* T) {
       RV[r] = (uint32_t)av; RP[r] = (uint32_t)ap;
     }
   }
-  uint2* out = T + ct_base(m, sz[0], sz[1], sz[2]);
+  uint2* out = rows + (size_t)ct_row(hdr, m, sz[0], sz[1], sz[2]) * CT;
   uint64_t av = 0, ap = 0;
   out[0] = make_uint2(0u, 0u);
-  for (int r = 1; r <= d; ++r) {
+  for (int r = 1; r <= d; ++r) {      // (every value < 2^32: at most 65^3 nodes per call, 64 calls)
     uint64_t fv, fp;
     if (m == 3) level_counts_f<PRUNE, INCL>(row[0], false, r, pf_row, fv, fp);
     else level_counts_f<PRUNE, INCL>(row[0], m == 1, r, pf_last, fv, fp);
@@ -828,7 +839,9 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       if (ctab != nullptr && m <= 3 && !traj) {                     // tabulated shape: two lookups
         const int lo = found ? (d > dwin ? zf + 1 : zf) : 1;
         if (lo <= d) {
-          const uint2* T = ctab + ct_base(m, row[0].size, m > 1 ? row[1].size : 0, m > 2 ? row[2].size : 0);
+          const uint32_t* hdr = (const uint32_t*)ctab;
+          const uint2* T = (const uint2*)((const unsigned char*)ctab + CT_HDR_BYTES) +
+                           (size_t)ct_row(hdr, m, row[0].size, m > 1 ? row[1].size : 0, m > 2 ? row[2].size : 0) * CT;
           const uint2 a = T[d], b = T[lo - 1];
           my_v += (uint64_t)(a.x - b.x) + (uint64_t)(d - lo + 1);    // + one root per call
           my_p += (uint64_t)(a.y - b.y);
@@ -1074,12 +1087,19 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     const unsigned same = __match_any_sync(EB_FULL, key) & active;
     if (lane < n && (same & lanemask_lt())) err_dup = lane;
   } else {
+    // within each 32-request slice by a match; against the earlier slices by
+    // a branch-free scan
 #pragma unroll
     for (int h = 0; h < NI; ++h) {
-      int i = lane + 32 * h;
-      if (i < n)
-        for (int j = 0; j < i; ++j)
-          if (a_id[j] == id_i[h]) { err_dup = min(err_dup, i); break; }
+      const int i = lane + 32 * h;
+      const int left = n - 32 * h;
+      const unsigned act_h = left >= 32 ? EB_FULL : (left > 0 ? ((1u << left) - 1u) : 0u);
+      const unsigned long long key = (i < n) ? (unsigned long long)id_i[h] : ~0ULL;
+      const unsigned same = __match_any_sync(EB_FULL, key) & act_h;
+      bool dup = i < n && (same & lanemask_lt());
+      if (h > 0 && i < n)
+        for (int j = 0; j < 32 * h; ++j) dup |= (a_id[j] == id_i[h]);
+      if (dup) err_dup = min(err_dup, i);
     }
   }
   err_dup = __reduce_min_sync(EB_FULL, err_dup);
@@ -1170,11 +1190,18 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
         }
         first = (peers & lanemask_lt()) == 0;
       } else {
+        // one branch-free pass: tau rank, class leadership, within-class rank
+        int kr = 0, earlier = 0;
         for (int j = 0; j < n; ++j) {
-          double tj = a_tau[j];
-          t += (tj > tau_i[h]) || (tj == tau_i[h] && a_id[j] < id_i[h]);
-          if (j < i && a_len[j] == len_i[h]) first = false;
+          const double tj = a_tau[j], kj = a_key[j];
+          const int idlt = (int)(a_id[j] < id_i[h]);
+          const int same = (int)(a_len[j] == len_i[h]);
+          t += (int)(tj > tau_i[h]) | ((int)(tj == tau_i[h]) & idlt);
+          earlier |= (int)(j < i) & same;
+          kr += same & ((int)(kj < key_i[h]) | ((int)(kj == key_i[h]) & idlt));
         }
+        first = !earlier;
+        kr_i[h] = kr;
       }
       t_i[h] = t;
       first_i[h] = first;
@@ -1226,17 +1253,11 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
           kr += (int)(kj < key_i[h]) | ((int)(kj == key_i[h]) & (int)(a_id[j] < id_i[h]));
         }
       } else {
-        for (int j = 0; j < n; ++j) {
-          unsigned fw = fmask[0];        // fmask[j >> 5] by selects (stays in registers)
+        // class index: leaders with a shorter output (kr came with the ranks)
 #pragma unroll
-          for (int q = 1; q < NI; ++q) fw = ((j >> 5) == q) ? fmask[q] : fw;
-          bool fj = (fw >> (j & 31)) & 1u;
-          g += fj && a_len[j] < len_i[h];
-          if (a_len[j] == len_i[h]) {
-            double kj = a_key[j];
-            kr += (kj < key_i[h]) || (kj == key_i[h] && a_id[j] < id_i[h]);
-          }
-        }
+        for (int q = 0; q < NI; ++q)
+          for (unsigned fm = fmask[q]; fm; fm &= fm - 1) g += a_len[32 * q + __ffs(fm) - 1] < len_i[h];
+        kr = kr_i[h];
       }
       gcls_i[h] = g;
       kr_i[h] = kr;
@@ -1353,7 +1374,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
                                        slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
                                        tot_v, tot_p,
                                        CountsMode{A.prm.exhaustive_counts != 0, c_start, c_list, o_key, o_dnt},
-                                       NI == 1 ? A.ctab : nullptr, sizes)) {
+                                       A.ctab, sizes)) {
       // leaf counts overflow the u32 unranking tables: hand the instance to
       // the literal walk (second pass of launch_dftsp)
       put_status(EB_STATUS_FALLBACK, -1);
@@ -1863,17 +1884,20 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   }
 #undef EB_PICKL3
   A.fallback_pass = 0;
-  if (algo == 2 && K <= 32 && !prm.exhaustive_counts) {
+  if (algo == 2 && K <= EB_MAX_K && !prm.exhaustive_counts) {
     const int v = !P ? 0 : (I ? 2 : 1);
     if (!h->ctab[v]) {
       // built once per handle and flag variant; synchronous, so kernels on
       // the other pipeline streams never see a partial table
       void* t = nullptr;
-      EB_CUDA(cudaMalloc(&t, CT_ENTRIES * sizeof(uint2)));
-      void (*bk)(uint2*) = !P ? count_table_kernel<false, false>
-                              : (I ? count_table_kernel<true, true> : count_table_kernel<true, false>);
-      const int nthr = 32 * 32 * 32 + 32 * 32 + 32;
-      bk<<<(nthr + 255) / 256, 256, 0, st>>>((uint2*)t);
+      EB_CUDA(cudaMalloc(&t, CT_HDR_BYTES + (size_t)CT_ROWS * CT * sizeof(uint2)));
+      uint32_t hdr[CT_HDR];
+      ct_header(hdr);
+      EB_CUDA(cudaMemcpyAsync(t, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
+      void (*bk)(const uint32_t*, uint2*) = !P ? count_table_kernel<false, false>
+                                               : (I ? count_table_kernel<true, true> : count_table_kernel<true, false>);
+      const int nthr = 64 * 64 * 64 + 64 * 64 + 64;
+      bk<<<(nthr + 255) / 256, 256, 0, st>>>((const uint32_t*)t, (uint2*)((unsigned char*)t + CT_HDR_BYTES));
       EB_CUDA(cudaGetLastError());
       h->launches += 1;
       EB_CUDA(cudaStreamSynchronize(st));
