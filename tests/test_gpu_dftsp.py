@@ -145,6 +145,26 @@ def test_gpu_edge_statuses():
     _assert_same(dev, orc, b, "edge statuses")
 
 
+def test_gpu_duplicate_ids_wide_instances():
+    """Instances of 33..64 requests (two per lane): duplicates inside the first
+    32, inside the rest, and across the two slices all report the oracle's
+    status and offending index (the smallest index with an earlier twin)."""
+    batch, ladders = random_batch(41, 40, k_min=40, k_max=64)
+    b = batch
+    ids = b.columns["id"]
+    for inst, (a, c) in {0: (3, 9), 1: (35, 50), 2: (4, 37), 3: (31, 32), 4: (0, 63), 5: (33, 34)}.items():
+        lo, hi = int(b.offsets[inst]), int(b.offsets[inst + 1])
+        if lo + c < hi:
+            ids[lo + c] = ids[lo + a]
+    lad = None
+    dev = search.solve_batch(b, ladder=lad)
+    orc = oracle.dftsp_batch(b, ladder=lad)
+    assert np.array_equal(dev.status, orc["status"])
+    assert np.array_equal(dev.error_index, orc["error_index"])
+    assert (dev.status == _lib.ERR_DUPLICATE_ID).sum() >= 4
+    _assert_same(dev, orc, b, "wide duplicates")
+
+
 def test_gpu_v2_table_overflow_falls_back_exactly():
     """Many classes with many members: u32 leaf counts overflow, the instance
     is re-run by the literal walk and still matches the oracle."""
