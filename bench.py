@@ -174,6 +174,15 @@ def profile_issue_pct():
         return None
 
 
+def profile_warp_inst():
+    """Warp instructions per instance of the search kernel (committed ncu capture)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_dftsp_summary.json")) as fh:
+            return json.load(fh).get("warp_instructions_per_instance")
+    except (OSError, ValueError):
+        return None
+
+
 def load_profile_traffic():
     """DRAM bytes per launch of the search kernel from the committed ncu capture (or None)."""
     p = os.path.join(ROOT, "profiles", "ncu_dftsp_summary.json")
@@ -183,6 +192,20 @@ def load_profile_traffic():
         return j.get("dram_bytes_per_launch"), j.get("instances_per_launch")
     except (OSError, ValueError):
         return None, None
+
+
+def issue_roofline(sms: int, f_mhz: float, n: int, per_launch_s: float):
+    """Warp-instruction issue rate of the search kernel against the SM issue
+    peak (4 schedulers x 1 warp-instruction per clock per SM): the bound the
+    kernel actually meets.  Instructions per instance come from the committed
+    ncu capture; the time is this run's."""
+    wi = profile_warp_inst()
+    if not wi:
+        return None
+    achieved = wi * n / per_launch_s / 1e9
+    peak = sms * 4 * f_mhz * 1e6 / 1e9
+    return {"achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "G warp-inst/s",
+            "frac": round(achieved / peak, 4), "warp_inst_per_instance_ncu": wi}
 
 
 def cpu_baseline(batch, sample: int, threads: int):
@@ -397,6 +420,7 @@ def main():
                                   "oracle on a 20k-instance sample of this workload; peak = SMs x 64 FP64 lanes x "
                                   "max SM clock (no measured FP64 peak in MEASURED_PEAKS.json)",
                      "issue_active_pct_ncu": profile_issue_pct(),
+                     "issue": issue_roofline(props.multi_processor_count, f_mhz, n, per_launch_s),
                      "issue_note": "SM issue-slot utilisation of the search kernel from the committed ncu capture "
                                    "(profiles/ncu_dftsp_summary.json): the path is instruction-issue bound "
                                    "(integer control + FP64 compare/accumulate)"},
