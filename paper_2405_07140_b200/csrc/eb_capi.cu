@@ -171,49 +171,79 @@ __global__ void uniform_offsets_kernel(int64_t ni, int64_t i0, int k, int64_t* _
     off[i] = (i0 + i) * k;
 }
 
-eb_requests upload_wire(Stage& S, const eb_requests_packed& r, int64_t lo, int64_t n) {
-  eb_requests d;
-  memset(&d, 0, sizeof(d));
-  const int32_t* id32 = r.id ? S.up(r.id + lo, n) : nullptr;
-  const uint16_t* p16 = S.up(r.prompt_tokens + lo, n);
-  const uint16_t* o16 = S.up(r.output_tokens + lo, n);
-  d.deadline_s = S.up(r.deadline_s + lo, n);
-  d.waiting_s = S.up(r.waiting_s + lo, n);
-  d.channel_gain = S.up(r.channel_gain + lo, n);
-  const double* pw = r.uplink_power_uniform ? S.up(r.uplink_power_w, 1) : S.up(r.uplink_power_w + lo, n);
-  int64_t* id64 = S.alloc<int64_t>(n);
-  int32_t* p32 = S.alloc<int32_t>(n);
-  int32_t* o32 = S.alloc<int32_t>(n);
-  double* pw64 = S.alloc<double>(n);
-  if (S.err) return d;
-  int blocks = (int)((n + 255) / 256);
-  if (blocks > 8 * S.h->num_sms) blocks = 8 * S.h->num_sms;
-  if (blocks < 1) blocks = 1;
-  widen_wire_kernel<<<blocks, 256, 0, S.st>>>(n, lo, id32, p16, o16, pw, r.uplink_power_uniform != 0, id64, p32,
-                                               o32, pw64);
-  ++S.h->launches;
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) { S.err = cuda_fail(e, "widen_wire_kernel"); return d; }
-  d.id = id64;
-  d.prompt_tokens = p32;
-  d.output_tokens = o32;
-  d.uplink_power_w = pw64;
-  return d;
-}
+// Upload policies of the DFTSP host pipeline: stage() issues the chunk's
+// host->device copies on the upload stream (into the input arena); widen()
+// runs on the chunk's compute stream once they have landed and returns the
+// eb_requests columns the search reads.
+struct WideUp {
+  const eb_requests* r;
+  static size_t row_bytes() { return 8 + 4 + 4 + 8 + 8 + 8 + 8 + 8; }
+  eb_requests stage(Stage& S, int64_t lo, int64_t n) const { return upload_req(S, *r, lo, n); }
+  eb_requests widen(Stage&, const eb_requests& d, int64_t, int64_t) const { return d; }
+};
+
+struct WireStaged {
+  const int32_t* id32;
+  const uint16_t *p16, *o16;
+  const double *dl, *w, *g, *pw;
+};
+
+struct WireUp {
+  const eb_requests_packed* r;
+  static size_t row_bytes() { return 4 + 2 + 2 + 8 + 8 + 8 + 8; }
+  WireStaged stage(Stage& S, int64_t lo, int64_t n) const {
+    WireStaged d;
+    d.id32 = r->id ? S.up(r->id + lo, n) : nullptr;
+    d.p16 = S.up(r->prompt_tokens + lo, n);
+    d.o16 = S.up(r->output_tokens + lo, n);
+    d.dl = S.up(r->deadline_s + lo, n);
+    d.w = S.up(r->waiting_s + lo, n);
+    d.g = S.up(r->channel_gain + lo, n);
+    d.pw = r->uplink_power_uniform ? S.up(r->uplink_power_w, 1) : S.up(r->uplink_power_w + lo, n);
+    return d;
+  }
+  eb_requests widen(Stage& S, const WireStaged& d, int64_t lo, int64_t n) const {
+    eb_requests q;
+    memset(&q, 0, sizeof(q));
+    int64_t* id64 = S.alloc<int64_t>(n);
+    int32_t* p32 = S.alloc<int32_t>(n);
+    int32_t* o32 = S.alloc<int32_t>(n);
+    double* pw64 = S.alloc<double>(n);
+    if (S.err) return q;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 8 * S.h->num_sms) blocks = 8 * S.h->num_sms;
+    if (blocks < 1) blocks = 1;
+    widen_wire_kernel<<<blocks, 256, 0, S.st>>>(n, lo, d.id32, d.p16, d.o16, d.pw, r->uplink_power_uniform != 0,
+                                                 id64, p32, o32, pw64);
+    ++S.h->launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { S.err = cuda_fail(e, "widen_wire_kernel"); return q; }
+    q.id = id64;
+    q.prompt_tokens = p32;
+    q.output_tokens = o32;
+    q.deadline_s = d.dl;
+    q.waiting_s = d.w;
+    q.channel_gain = d.g;
+    q.uplink_power_w = pw64;
+    return q;
+  }
+};
 
 bool req_complete(const eb_requests& r, bool need_tol) {
   return r.id && r.prompt_tokens && r.output_tokens && r.deadline_s && r.waiting_s && r.channel_gain &&
          r.uplink_power_w && (!need_tol || r.tolerance);
 }
 
-// Host-memory DFTSP: instance chunks pipelined over the handle's three
-// staging streams (H2D of chunk c+1 overlaps the search of chunk c and the
-// D2H of chunk c-1).  `upload(S, R0, nr)` stages request rows [R0, R0+nr)
-// and returns their device columns (wide or wire format).
+// Host-memory DFTSP: instance chunks pipelined over an upload stream and the
+// handle's three compute streams.  Every chunk's inputs get their own slice
+// of the input arena, so the uploads run back to back on `up` (the PCIe
+// bound) while chunk c computes on pipe[c % 3], waiting only for its own
+// copies; outputs go back on the compute stream (the other copy direction).
+// `upload` stages request rows [R0, R0+nr) (WideUp / WireUp).
 template <typename Upload>
 int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const eb_search_params& prm, int64_t n,
                         const int64_t* offsets, const int32_t* ctx_index, int K, int64_t n_wide,
-                        const eb_dftsp_result& out, Upload upload) {
+                        const eb_dftsp_result& out, const Upload& upload) {
   // offsets == NULL: every instance has K requests (wire format only)
   auto off_at = [&](int64_t i) -> int64_t { return offsets ? offsets[i] : i * (int64_t)K; };
   // Chunking: the first chunk's copy and the last chunk's search are the
@@ -246,6 +276,7 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
   // events a caller records on that stream bracket the whole host->host call.
   EB_CUDA(cudaEventRecord(h->ev[0], h->stream));
   for (int i = 0; i < 3; ++i) EB_CUDA(cudaStreamWaitEvent(h->pipe[i], h->ev[0], 0));
+  EB_CUDA(cudaStreamWaitEvent(h->up, h->ev[0], 0));
   // context table once per pipe stream (tiny)
   std::vector<Stage*> stages;
   int rc = EB_OK;
@@ -283,15 +314,45 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
       h->arena_bytes[sidx] = bytes;
     }
   }
+  // input arena: every chunk's uploaded inputs (offsets, context index,
+  // trajectory offsets, request columns), 256 B slack per buffer
+  std::vector<size_t> in_off(nchunks + 1, 0);
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t i0 = cut[c], i1 = cut[c + 1];
+    const size_t b = 16 * 256 + (size_t)(i1 - i0 + 1) * 20 + (size_t)(off_at(i1) - off_at(i0)) * Upload::row_bytes();
+    in_off[c + 1] = in_off[c] + ((b + 255) & ~(size_t)255);     // slices stay 256 B aligned
+  }
+  if (rc == EB_OK && h->in_arena_bytes < in_off[nchunks]) {
+    if (h->in_arena) cudaFreeAsync(h->in_arena, h->up);
+    h->in_arena = nullptr;
+    h->in_arena_bytes = 0;
+    cudaError_t e = cudaMallocAsync(&h->in_arena, in_off[nchunks], h->up);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocAsync(input arena)");
+    else h->in_arena_bytes = in_off[nchunks];
+  }
   for (int c = 0; c < nchunks && rc == EB_OK; ++c) {
     cudaStream_t st = h->pipe[c % 3];
     Stage* S = new Stage(h, st, h->arena[c % 3], h->arena_bytes[c % 3]);
     stages.push_back(S);
+    Stage* U = new Stage(h, h->up, (unsigned char*)h->in_arena + in_off[c], in_off[c + 1] - in_off[c]);
+    stages.push_back(U);
     const int64_t i0 = cut[c], i1 = cut[c + 1], ni = i1 - i0;
     const int64_t R0 = off_at(i0), R1 = off_at(i1), nr = R1 - R0;
+    // uploads (stream `up`), then the compute stream waits for them
+    const int64_t* d_off_up = offsets ? U->up(offsets + i0, (size_t)ni + 1) : nullptr;
+    const int32_t* d_ci = ctx_index ? U->up(ctx_index + i0, (size_t)ni) : nullptr;
+    const auto staged = upload.stage(*U, R0, nr);
+    const int64_t* d_traj_off = prm.collect_trajectory ? U->up(out.traj_offsets + i0, (size_t)ni + 1) : nullptr;
+    if (U->err) { rc = U->err; break; }
+    {
+      cudaEvent_t ev = h->cev[c % 64];
+      cudaError_t e = cudaEventRecord(ev, h->up);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev, 0);
+      if (e != cudaSuccess) { rc = cuda_fail(e, "chunk upload event"); break; }
+    }
     const int64_t* d_off;
     if (offsets) {
-      d_off = S->up(offsets + i0, (size_t)ni + 1);
+      d_off = d_off_up;
     } else {
       int64_t* o = S->alloc<int64_t>((size_t)ni + 1);
       if (o) {
@@ -304,8 +365,7 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
       }
       d_off = o;
     }
-    const int32_t* d_ci = ctx_index ? S->up(ctx_index + i0, (size_t)ni) : nullptr;
-    eb_requests d_req = upload(*S, R0, nr);
+    eb_requests d_req = upload.widen(*S, staged, R0, nr);
     eb_dftsp_result d_out;
     memset(&d_out, 0, sizeof(d_out));
     d_out.status = S->alloc<int32_t>(ni);
@@ -322,7 +382,7 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
     if (prm.collect_trajectory) {
       T0 = out.traj_offsets[i0];
       int64_t nt = out.traj_offsets[i1] - T0;
-      d_out.traj_offsets = S->up(out.traj_offsets + i0, (size_t)ni + 1);
+      d_out.traj_offsets = d_traj_off;
       d_out.traj = S->alloc<int64_t>((size_t)nt * 4);
       d_out.traj_len = S->out(out.traj_len, ni);
     }
@@ -356,7 +416,10 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
     cudaEventRecord(h->ev[i], h->pipe[i]);
     cudaStreamWaitEvent(h->stream, h->ev[i], 0);
   }
+  cudaEventRecord(h->cev[0], h->up);
+  cudaStreamWaitEvent(h->stream, h->cev[0], 0);
   for (int i = 0; i < 3; ++i) cudaStreamSynchronize(h->pipe[i]);
+  cudaStreamSynchronize(h->up);
   return rc;
 }
 
@@ -414,6 +477,8 @@ int32_t eb_handle_create(int32_t device, eb_handle** out) {
     EB_CUDA(cudaStreamCreateWithFlags(&h->pipe[i], cudaStreamNonBlocking));
     EB_CUDA(cudaEventCreateWithFlags(&h->ev[i], cudaEventDisableTiming));
   }
+  EB_CUDA(cudaStreamCreateWithFlags(&h->up, cudaStreamNonBlocking));
+  for (int i = 0; i < 64; ++i) EB_CUDA(cudaEventCreateWithFlags(&h->cev[i], cudaEventDisableTiming));
   EB_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -434,6 +499,9 @@ int32_t eb_handle_destroy(eb_handle* h) {
   cudaDeviceSynchronize();
   if (h->own_stream) cudaStreamDestroy(h->stream);
   for (int i = 0; i < 3; ++i) { cudaStreamDestroy(h->pipe[i]); cudaEventDestroy(h->ev[i]); }
+  cudaStreamDestroy(h->up);
+  for (int i = 0; i < 64; ++i) cudaEventDestroy(h->cev[i]);
+  if (h->in_arena) cudaFree(h->in_arena);
   if (h->dscratch) cudaFree(h->dscratch);
   if (h->pinned) cudaFreeHost(h->pinned);
   for (int i = 0; i < 3; ++i) {
@@ -505,7 +573,7 @@ int32_t eb_dftsp_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, cons
   if (K > EB_MAX_K_DFTSP) K = EB_MAX_K_DFTSP;
   if (K < 1) K = 1;
   return dftsp_host_pipeline(h, ctxs, n_ctx, *prm, n, b->offsets, b->ctx_index, K, n_wide, *out,
-                             [&](Stage& S, int64_t R0, int64_t nr) { return upload_req(S, b->req, R0, nr); });
+                             WideUp{&b->req});
 }
 
 int32_t eb_dftsp_batch_packed(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_search_params* prm,
@@ -525,7 +593,7 @@ int32_t eb_dftsp_batch_packed(eb_handle* h, const eb_context* ctxs, int32_t n_ct
   EB_CUDA(cudaSetDevice(h->device));
   if (b->n_inst == 0) return EB_OK;
   return dftsp_host_pipeline(h, ctxs, n_ctx, *prm, b->n_inst, b->offsets, b->ctx_index, b->k_max, 0, *out,
-                             [&](Stage& S, int64_t R0, int64_t nr) { return upload_wire(S, r, R0, nr); });
+                             WireUp{&r});
 }
 
 int32_t eb_dfs_single(eb_handle* h, int32_t z, int32_t n_cls, const int32_t* sizes, const int32_t* lengths,

@@ -79,6 +79,8 @@ struct eb_handle {
   bool own_stream;
   cudaStream_t pipe[3];      // staging pipeline streams (host-memory calls)
   cudaEvent_t ev[3];
+  cudaStream_t up;           // host->device uploads of the DFTSP pipeline, back to back
+  cudaEvent_t cev[64];       // per-chunk "inputs landed" events (reused modulo 64)
   int num_sms;
   int64_t launches;
   // device scratch (grow-only)
@@ -94,6 +96,9 @@ struct eb_handle {
   // chunk c and chunk c+3 share a stream, so reuse is stream-ordered)
   void* arena[3];
   size_t arena_bytes[3];
+  // inputs of every chunk of a call (uploads never wait for a buffer to free)
+  void* in_arena;
+  size_t in_arena_bytes;
 };
 
 namespace eb {
