@@ -5,8 +5,8 @@
            pkg/scenarios (captured by tests/golden/make_golden.py): DFTSP and
            brute force, parity vs the reference's recorded outputs
   config3  K = 10..40 sweep x deadline scale x tolerance cap (w8a16): DFTSP
-           instances/s per K, plus the StB / NoB batching baselines on the same
-           queues (scheduled counts)
+           instances/s per K and mean z, beside the StB / NoB batching baselines
+           on the same queues (mean scheduled and on-time requests)
   config4  brute force 2^K, K = 28..32: level-by-level rank-range search
            (brute.solve_sharded, world 1 on this GPU; the same driver shards by
            rank over NCCL), z cross-checked against DFTSP (optimality)
@@ -140,6 +140,67 @@ def config1(threads):
             "brute_mismatches_vs_reference": bad_ex}
 
 
+def batching_baselines(b, w):
+    """StB and NoB on the same queues (the instances' candidates, FIFO in row
+    order), on the device: mean on-time requests per instance.  StB: b =
+    static_batch_size (baselines.py:51-65), FIFO admission (eb_stb_batch),
+    then the batch's own cost (eb_batch_cost_batch); a member is on time when
+    waiting + slots + latency <= deadline (sim.py:369-385).  NoB: every device
+    idle, one request per device (eb_nob_batch), on time when waiting +
+    completion <= deadline."""
+    import ctypes
+    h = _lib.handle(0)
+    ref = lambda x: ctypes.cast(ctypes.pointer(x), ctypes.c_void_p)  # noqa: E731
+    n, nr = b.n_inst, b.n_req
+    ctx = b.contexts
+    slots = float(ctx["uplink_slot_s"][0] + ctx["downlink_slot_s"][0])
+    sl = np.full(len(ctx), w.epoch_s)
+    smax = np.full(len(ctx), max(w.prompts), np.int64)
+    nmax = np.full(len(ctx), max(w.outputs), np.int64)
+    bsz = np.zeros(len(ctx), np.int64)
+    _lib.check(h.lib.eb_static_batch_size_batch(h.ptr, ctx.ctypes.data, len(ctx), sl.ctypes.data, smax.ctypes.data,
+                                                nmax.ctypes.data, bsz.ctypes.data, _lib.EB_MEM_HOST), "static_b")
+    bb = np.ascontiguousarray(bsz[b.ctx_index])
+    st = np.zeros(n, np.int32)
+    sel = np.zeros(nr, np.uint8)
+    bs = b.struct()
+    _lib.check(h.lib.eb_stb_batch(h.ptr, ctx.ctypes.data, len(ctx), ref(bs), bb.ctypes.data, 1, st.ctypes.data,
+                                  sel.ctypes.data, _lib.EB_MEM_HOST), "stb")
+    rows = np.nonzero(sel)[0]
+    owner = np.searchsorted(b.offsets, rows, side="right") - 1
+    plan_off = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(owner, minlength=n), out=plan_off[1:])
+    pr = np.ascontiguousarray(b.columns["prompt_tokens"][rows])
+    ou = np.ascontiguousarray(b.columns["output_tokens"][rows])
+    padded = np.zeros(n, np.int64)
+    np.maximum.at(padded, owner, pr.astype(np.int64))
+    cost = np.zeros((n, 2))
+    pc = np.ascontiguousarray(b.ctx_index)
+    _lib.check(h.lib.eb_batch_cost_batch(h.ptr, ctx.ctypes.data, len(ctx), n, plan_off.ctypes.data, pr.ctypes.data,
+                                         ou.ctypes.data, padded.ctypes.data, None, pc.ctypes.data, cost.ctypes.data,
+                                         _lib.EB_MEM_HOST), "batch_cost")
+    lat = cost[owner, 1]
+    w_s, dl = b.columns["waiting_s"][rows], b.columns["deadline_s"][rows]
+    stb_on = np.bincount(owner[(w_s + slots + lat) - dl <= 1e-9 * np.maximum(1.0, np.abs(dl))], minlength=n)
+    now = np.zeros(n)
+    G = int(ctx["gpu_count"].max())
+    busy = np.zeros((n, G))
+    st2 = np.zeros(n, np.int32)
+    act = np.zeros(nr, np.int8)
+    comp = np.zeros(nr)
+    order = np.zeros(nr, np.int32)
+    _lib.check(h.lib.eb_nob_batch(h.ptr, ctx.ctypes.data, len(ctx), ref(bs), now.ctypes.data, 1, None, G,
+                                  busy.ctypes.data, st2.ctypes.data, act.ctypes.data, comp.ctypes.data,
+                                  order.ctypes.data, _lib.EB_MEM_HOST), "nob")
+    r2 = np.nonzero(act == 1)[0]
+    o2 = np.searchsorted(b.offsets, r2, side="right") - 1
+    tot = b.columns["waiting_s"][r2] + comp[r2]
+    d2 = b.columns["deadline_s"][r2]
+    nob_on = np.bincount(o2[tot - d2 <= 1e-9 * np.maximum(1.0, np.abs(d2))], minlength=n)
+    return {"stb_b": int(bsz[0]), "stb_scheduled_mean": float(sel.sum() / n), "stb_on_time_mean": float(stb_on.mean()),
+            "nob_scheduled_mean": float((act == 1).sum() / n), "nob_on_time_mean": float(nob_on.mean())}
+
+
 def config3(threads, n_per_k):
     out = []
     for K in (10, 15, 20, 25, 30, 35, 40):
@@ -153,7 +214,8 @@ def config3(threads, n_per_k):
             kr, er = device_rates(b, (128, 256, 512))
             cr, orc = cpu_rate(b, (128, 256, 512), 2000 if K <= 25 else 300, threads)
             ok = bool(np.array_equal(orc["nodes_visited"], res.nodes_visited[:len(orc["nodes_visited"])]))
-            out.append({"K": K, "deadline_scale": ds, "tolerance_cap": tc, "instances": n,
+            base = batching_baselines(b, w)
+            out.append({"K": K, "deadline_scale": ds, "tolerance_cap": tc, "instances": n, **base,
                         "kernel_inst_per_s": round(kr, 1), "wire_e2e_inst_per_s": round(er, 1),
                         "api_inst_per_s": round(n / dt, 1), "mean_z": float(res.z_found.mean()),
                         "mean_nodes_visited": float(res.nodes_visited.mean()), "cpu_port_inst_per_s": round(cr, 1),
