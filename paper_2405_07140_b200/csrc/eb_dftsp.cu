@@ -83,9 +83,12 @@ __host__ __device__ inline Lay make_lay(int K, int G, bool exact, bool v2) {
   L.sol = take(K);
   if (v2) {
     const int lvls = G > 1 ? G - 1 : 1;
-    L.pq = take(4 * (size_t)K * lvls * (K + 2));
+    // the unranking tables (search) and the winner's count rows (counts
+    // phase, after the search) share one region
+    const size_t pq_bytes = 4 * (size_t)K * lvls * (K + 2), pf_bytes = 16 * (size_t)G * (K + 1);
+    L.pq = take(pq_bytes > pf_bytes ? pq_bytes : pf_bytes);
+    L.pf = L.pq;
     L.pre = take(4 * 64 + 8 * 32);
-    L.pf = take(16 * (size_t)G * (K + 1));
   } else {
     L.pq = L.pre = L.pf = 0;
   }
@@ -1873,10 +1876,25 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   if (algo == 2) {
     // lockstep blocks: up to 16 warps (one instance each) sharing phases
     // (EB_LOCK_WARPS overrides the width, for tuning)
-    int cap_w = 8;   // measured: 4 -> 44.4, 8 -> 51.6, 12 -> 40.8, 16 -> 50.4 M inst/s (config 2)
+    // Block width: the most resident warps per SM (shared memory: 228 KB
+    // per SM, 1 KB reserved per block; registers: 16 warps at 128 each),
+    // preferring wider blocks (measured at K=20: 4 -> 44.4, 8 -> 51.6,
+    // 16 -> 50.4 M inst/s).  Wide instances (K = 21..64) thus get e.g. two
+    // 5-warp blocks instead of one 8-warp block.
+    int cap_w = 8;
     if (const char* e = getenv("EB_LOCK_WARPS")) { int v = atoi(e); if (v >= 1 && v <= 16) cap_w = v; }
-    warps = (int)(smem_cap / A.warp_bytes);
-    if (warps > cap_w) warps = cap_w;
+    {
+      const size_t sm_bytes = 228 * 1024;
+      int best_w = 1, best_res = 0;
+      for (int w = 1; w <= cap_w; ++w) {
+        if (A.warp_bytes * w > smem_cap) break;
+        int blocks = (int)(sm_bytes / (A.warp_bytes * w + 1024));
+        if (blocks > 16 / w) blocks = 16 / w;
+        const int res = blocks * w;
+        if (res >= best_res) { best_res = res; best_w = w; }
+      }
+      warps = best_w;
+    }
     smem = A.warp_bytes * warps;
     if (K <= 32) { EB_PICKL3(1) } else { EB_PICKL3(2) }
   } else {
