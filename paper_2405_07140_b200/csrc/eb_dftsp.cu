@@ -76,8 +76,14 @@ __host__ __device__ inline Lay make_lay(int K, int G, bool exact, bool v2) {
   L.c_list = take(K);
   L.sizes = take((size_t)K * G); L.ncls = take(K); L.lvl = take(8 * (size_t)K * G);
   L.T = K * (K + 1) / 2 + K * G;
-  L.t_up = take(8 * (size_t)L.T); L.t_dn = take(8 * (size_t)L.T);
-  L.t_tau = exact ? take(8 * (size_t)L.T) : 0;
+  if (!v2) {
+    L.t_up = take(8 * (size_t)L.T); L.t_dn = take(8 * (size_t)L.T);
+    L.t_tau = exact ? take(8 * (size_t)L.T) : 0;
+  } else {
+    // the leaf-parallel search folds each class prefix on the fly (a leaf
+    // batch per instance, typically); no per-width prefix tables
+    L.t_up = L.t_dn = L.t_tau = 0;
+  }
   if (!v2) { L.ring_v = take(8 * RING); L.ring_p = take(8 * RING); L.ring_done = take(RING); }
   else { L.ring_v = L.ring_p = L.ring_done = 0; }
   L.sol = take(K);
@@ -85,8 +91,13 @@ __host__ __device__ inline Lay make_lay(int K, int G, bool exact, bool v2) {
     const int lvls = G > 1 ? G - 1 : 1;
     // the unranking tables (search) and the winner's count rows (counts
     // phase, after the search) share one region
+    // the unranking tables (search), then the count rows of the lanes =
+    // widths pass and the winner's count rows (counts phase) share a region
     const size_t pq_bytes = 4 * (size_t)K * lvls * (K + 2), pf_bytes = 16 * (size_t)G * (K + 1);
-    L.pq = take(pq_bytes > pf_bytes ? pq_bytes : pf_bytes);
+    const size_t rows_bytes = 32 * 2 * 4 * (size_t)(K + 1);
+    size_t sc = pq_bytes > pf_bytes ? pq_bytes : pf_bytes;
+    if (rows_bytes > sc) sc = rows_bytes;
+    L.pq = take(sc);
     L.pf = L.pq;
     L.pre = take(4 * 64 + 8 * 32);
   } else {
@@ -645,18 +656,6 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
                       ((uint64_t)__reduce_or_sync(EB_FULL, (unsigned)(bit >> 32)) << 32);
       want &= ~built;
       bool ok = true;
-      if (want) {
-        // prefix tables of the new widths: lanes = (width, class) pairs
-        const int nwant = __popcll(want);
-        for (int w = lane; w < nwant * Gi; w += 32) {
-          const int wi = w / Gi, g = w % Gi;
-          uint64_t mm = want;
-          for (int q = 0; q < wi; ++q) mm &= mm - 1;               // drop the wi lowest widths
-          build_width_tables<EXACT>(__ffsll((long long)mm), g, Gi, sizes, cm.c_start, cm.c_list, cm.o_key,
-                                    cm.o_dnt, o_tau, (double*)t_up, (double*)t_dn, (double*)t_tau);
-        }
-        __syncwarp();
-      }
       while (want) {
         const int dd = __ffsll((long long)want);
         want &= want - 1;
@@ -752,11 +751,24 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
             cc = r - xa;
           }
           if (cc) { setV(V0, V1, k, cc); klast = k; }
-          u = add(u, t_up[li.off + cc]);                           // up_acc + up[k][x]
-          dl = add(dl, t_dn[li.off + cc]);
+          // SearchTables.build's up[k][cc] / dn[k][cc] / tau_min_prefix[k][cc]
+          // (dftsp.py:119-128): the same sequential folds over the class's
+          // first cc members among the dd first by tau, in key order
+          double cu = 0.0, cdn = 0.0, tm = INF;
+          for (int p = cm.c_start[li.g], taken = 0; taken < cc; ++p) {
+            const int t = cm.c_list[p];
+            if (t < dd) {
+              cu = add(cu, cm.o_key[t]);
+              cdn = add(cdn, cm.o_dnt[t]);
+              if (EXACT) tm = pymin(tm, o_tau[t]);
+              ++taken;
+            }
+          }
+          u = add(u, cu);                                          // up_acc + up[k][x]
+          dl = add(dl, cdn);
           mem += (int64_t)cc * c_len[li.g];
           lat = add(lat, mul(i2d(cc), c_w[li.g]));
-          if (EXACT && cc) tau = pymin(tau, t_tau[li.off + cc]);
+          if (EXACT && cc) tau = pymin(tau, tm);
           r -= cc;
         }
         const double cap = EXACT ? pymin(sub(tau, k3z), slot_cap) : pymin(sub(o_tau[dd - 1], k3z), slot_cap);
@@ -826,7 +838,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
   uint64_t my_v = 0, my_p = 0;
   {
     bool ovf = false;
-    uint32_t* rows = (uint32_t*)(smem + L.t_up);
+    uint32_t* rows = (uint32_t*)(smem + L.pq);    // unranking tables are dead now
     const int W2 = 2 * (n + 1);
     for (int dbase = found ? zf : 1; dbase <= n; dbase += 32) {
       const int d = dbase + lane;
