@@ -1318,21 +1318,26 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
 
   // ---------------- per pool width d: class sizes, levels, tables --------
   const int nDG = n * Gi;
-  if constexpr (NI == 1) {
+  (void)nDG;
+  {
     // sizes[d][g] = members of class g among the d first in tau order: one
-    // ballot per class over lanes = tau ranks, then lanes = d count bits < d
-    const int gt = lane < n ? o_g[lane] : -1;
-    const unsigned below = (lane < n) ? ((2u << lane) - 1u) : 0u;     // ranks 0 .. d-1, d = lane + 1
-    for (int g = 0; g < Gi; ++g) {
-      const unsigned mg = __ballot_sync(EB_FULL, gt == g);
-      if (lane < n) sizes[lane * Gi + g] = (uint8_t)__popc(mg & below);
-    }
-  } else {
-    for (int w = lane; w < nDG; w += 32) {
-      int d = w / Gi + 1, g = w % Gi;
-      int cnt = 0, b = c_start[g], e = c_start[g + 1];
-      for (int q = b; q < e; ++q) cnt += c_list[q] < d;
-      sizes[(d - 1) * Gi + g] = (uint8_t)cnt;
+    // ballot per class and 32-rank slice over lanes = tau ranks, then lanes =
+    // d count the bits below d (earlier slices whole)
+#pragma unroll
+    for (int h = 0; h < NI; ++h) {
+      const int t = lane + 32 * h;                            // tau rank; width d = t + 1
+      const int gt = t < n ? o_g[t] : -1;
+      const unsigned below = (t < n) ? ((2u << lane) - 1u) : 0u;
+      for (int g = 0; g < Gi; ++g) {
+        int full = 0;                                         // class g in slices before h
+#pragma unroll
+        for (int q = 0; q < h; ++q) {
+          const int tq = lane + 32 * q;
+          full += __popc(__ballot_sync(EB_FULL, tq < n && o_g[tq] == g));
+        }
+        const unsigned mg = __ballot_sync(EB_FULL, gt == g);
+        if (t < n) sizes[t * Gi + g] = (uint8_t)(full + __popc(mg & below));
+      }
     }
   }
   __syncwarp();
@@ -1510,6 +1515,41 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
           int base = 0;
           for (int k2 = 0; k2 < kk && k2 <= kwin; ++k2) base += getV(W0, W1, k2);
           sol[base + rk] = (uint8_t)t;
+        }
+      }
+    } else if constexpr (NI == 2) {
+      // the same over two 32-position slices of the class lists
+      int tt[2], gg[2];
+      bool inb[2];
+      unsigned inm[2], present = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = lane + 32 * h;
+        tt[h] = p < n ? c_list[p] : 0;
+        gg[h] = p < n ? o_g[tt[h]] : 0;
+        inb[h] = p < n && tt[h] < dwin;
+        inm[h] = __ballot_sync(EB_FULL, inb[h]);
+        present |= __reduce_or_sync(EB_FULL, inb[h] ? (1u << gg[h]) : 0u);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!inb[h]) continue;
+        const int p = lane + 32 * h, g = gg[h], cs = c_start[g];
+        int rk = 0;                                    // qualifying positions in [cs, p)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+          const int lo = max(cs - 32 * w, 0), hi = min(p - 32 * w, 32);
+          if (hi > lo) {
+            const unsigned upto = hi == 32 ? EB_FULL : ((1u << hi) - 1u);
+            rk += __popc(inm[w] & upto & ~((1u << lo) - 1u));
+          }
+        }
+        const int kk = __popc(present & ((1u << g) - 1u));
+        const int cnt = (kk <= kwin) ? getV(W0, W1, kk) : 0;
+        if (rk < cnt) {
+          int base = 0;
+          for (int k2 = 0; k2 < kk && k2 <= kwin; ++k2) base += getV(W0, W1, k2);
+          sol[base + rk] = (uint8_t)tt[h];
         }
       }
     } else if (lane == 0) {
