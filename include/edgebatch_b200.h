@@ -265,6 +265,15 @@ int32_t eb_exhaustive_level_range(eb_handle *h, const eb_context *ctx,
                                   int64_t rank_lo, int64_t rank_hi,
                                   int64_t *first_rank);
 
+/* Levels worth searching for one instance (host memory, synchronous): bit
+ * z-1 of *live_mask is set unless the sound level bounds the range search
+ * applies (minimum memory, compute time, uplink, downlink and deadline over
+ * all size-z subsets) prove that no size-z subset passes check_direct.  A
+ * sharded search can skip the clear levels: eb_exhaustive_level_range would
+ * return -1 for them. */
+int32_t eb_exhaustive_live_levels(eb_handle *h, const eb_context *ctx, int32_t k,
+                                  const eb_requests *req, uint64_t *live_mask);
+
 /* ---- K2: batched feasibility / cost ----------------------------------- */
 /* check_direct(subset, ctx, padded_len) feasibility.py:192-223 for n_sub
  * subsets.  Subset s = request rows members[sub_off[s] .. sub_off[s+1]) of

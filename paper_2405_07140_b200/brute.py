@@ -78,15 +78,29 @@ def device_level_range(ctx_rec: np.ndarray, cols: dict, device=None):
     rs = requests_struct(cols)
     ref = ctypes.cast(ctypes.pointer(rs), ctypes.c_void_p)
 
-    def level(z: int, lo: int, hi: int) -> int:
-        out = ctypes.c_int64(-1)
-        code = h.lib.eb_exhaustive_level_range(h.ptr, ctx_rec.ctypes.data, n, ref, z, lo, hi, ctypes.byref(out))
+    def raise_link(code):
         if code in (_lib.ERR_UPLINK_EFF_ZERO, _lib.ERR_DOWNLINK_EFF_ZERO):
             raise ValueError("uplink spectral efficiency is zero" if code == _lib.ERR_UPLINK_EFF_ZERO
                              else "downlink spectral efficiency is zero")
+
+    # levels the sound bounds do not refute (the range search would return -1
+    # for the others without enumerating anything)
+    live = ctypes.c_uint64(0)
+    code = h.lib.eb_exhaustive_live_levels(h.ptr, ctx_rec.ctypes.data, n, ref, ctypes.byref(live))
+    raise_link(code)
+    _lib.check(code, "eb_exhaustive_live_levels")
+    live_mask = int(live.value)
+
+    def level(z: int, lo: int, hi: int) -> int:
+        if not (live_mask >> (z - 1)) & 1:
+            return -1
+        out = ctypes.c_int64(-1)
+        code = h.lib.eb_exhaustive_level_range(h.ptr, ctx_rec.ctypes.data, n, ref, z, lo, hi, ctypes.byref(out))
+        raise_link(code)
         _lib.check(code, "eb_exhaustive_level_range")
         return int(out.value)
 
+    level.live_mask = live_mask
     return level
 
 

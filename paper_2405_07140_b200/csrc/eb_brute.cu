@@ -58,6 +58,14 @@ struct Members {
   int64_t lo_far[EB_MAX_K + 1];
   int64_t lo_n[EB_MAX_K + 1];
   double lo_a[EB_MAX_K + 1], lo_b[EB_MAX_K + 1];
+  // deadline bound: bit z-1 set when some size-z subset may meet every
+  // member's deadline under its least compute time (build_level_bounds)
+  unsigned long long lat_ok;
+  // scratch of the bound build: far-ascending order, slack-descending rank
+  uint8_t far_order[EB_MAX_K], slack_rank[EB_MAX_K];
+  int64_t srt_far[EB_MAX_K];
+  int32_t srt_n[EB_MAX_K];
+  double srt_a[EB_MAX_K], srt_b[EB_MAX_K];
 };
 
 // true only if leq(a, b) is false for every a >= a_lo (leq is monotone in a);
@@ -78,30 +86,75 @@ __device__ __forceinline__ bool level_infeasible(const Members& S, int z) {
   if (S.has_cap && fails_margin(cs, S.cap_s)) return true;
   if (fails_margin(mul(S.lo_a[z], 0.999999999999), 1.0)) return true;
   if (fails_margin(mul(S.lo_b[z], 0.999999999999), 1.0)) return true;
-  return false;
+  return !((S.lat_ok >> (z - 1)) & 1ULL);
 }
 
-// Sorted-prefix bounds (one thread; n <= 64).
+// Level bounds, block-cooperative (every thread calls it; n <= 64).
+//  * Sorted prefixes: the z smallest far / n / uplink / downlink terms
+//    (rank sort, one thread per member, then one thread folds the prefixes).
+//  * Deadline bound: a feasible subset S has a member j with the least slack
+//    (dl - ws; the largest slack rank in S), and every other member ranks
+//    above it.  Its compute time is at least that of z * fi + far_j + the
+//    z - 1 smallest far terms among the members ranked above j, and j must
+//    meet its deadline (and the slot cap) under it.  Thread j walks the
+//    far-ascending order once, adding the members ranked above it, and marks
+//    every z whose bound passes; a level no member marks is infeasible.  The
+//    FLOP sums are exact integers and the checks are the monotone leq of
+//    check_direct with the fails_margin slack, so the bound is sound.
 __device__ void build_level_bounds(Members& S) {
   const int n = S.n;
-  int64_t f[EB_MAX_K];
-  int32_t q[EB_MAX_K];
-  double a[EB_MAX_K], b[EB_MAX_K];
-  for (int i = 0; i < n; ++i) { f[i] = S.far[i]; q[i] = S.nout[i]; a[i] = S.a[i]; b[i] = S.b[i]; }
-  for (int i = 1; i < n; ++i)
-    for (int j = i; j > 0; --j) {
-      if (f[j] < f[j - 1]) { int64_t t = f[j]; f[j] = f[j - 1]; f[j - 1] = t; }
-      if (q[j] < q[j - 1]) { int32_t t = q[j]; q[j] = q[j - 1]; q[j - 1] = t; }
-      if (a[j] < a[j - 1]) { double t = a[j]; a[j] = a[j - 1]; a[j - 1] = t; }
-      if (b[j] < b[j - 1]) { double t = b[j]; b[j] = b[j - 1]; b[j - 1] = t; }
+  if (threadIdx.x == 0) S.lat_ok = 0ULL;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int rf = 0, rn = 0, ra = 0, rb = 0, rs = 0;
+    const double si = sub(S.dl[i], S.ws[i]);
+    for (int j = 0; j < n; ++j) {
+      const int jl = j < i;
+      rf += (S.far[j] < S.far[i]) | ((S.far[j] == S.far[i]) & jl);
+      rn += (S.nout[j] < S.nout[i]) | ((S.nout[j] == S.nout[i]) & jl);
+      ra += (S.a[j] < S.a[i]) | ((S.a[j] == S.a[i]) & jl);
+      rb += (S.b[j] < S.b[i]) | ((S.b[j] == S.b[i]) & jl);
+      const double sj = sub(S.dl[j], S.ws[j]);
+      rs += (sj > si) | ((sj == si) & jl);
     }
-  S.lo_far[0] = 0; S.lo_n[0] = 0; S.lo_a[0] = 0.0; S.lo_b[0] = 0.0;
-  for (int z = 1; z <= n; ++z) {
-    S.lo_far[z] = S.lo_far[z - 1] + f[z - 1];
-    S.lo_n[z] = S.lo_n[z - 1] + q[z - 1];
-    S.lo_a[z] = add(S.lo_a[z - 1], a[z - 1]);
-    S.lo_b[z] = add(S.lo_b[z - 1], b[z - 1]);
+    S.srt_far[rf] = S.far[i];
+    S.far_order[rf] = (uint8_t)i;
+    S.srt_n[rn] = S.nout[i];
+    S.srt_a[ra] = S.a[i];
+    S.srt_b[rb] = S.b[i];
+    S.slack_rank[i] = (uint8_t)rs;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S.lo_far[0] = 0; S.lo_n[0] = 0; S.lo_a[0] = 0.0; S.lo_b[0] = 0.0;
+    for (int z = 1; z <= n; ++z) {
+      S.lo_far[z] = S.lo_far[z - 1] + S.srt_far[z - 1];
+      S.lo_n[z] = S.lo_n[z - 1] + S.srt_n[z - 1];
+      S.lo_a[z] = add(S.lo_a[z - 1], S.srt_a[z - 1]);
+      S.lo_b[z] = add(S.lo_b[z - 1], S.srt_b[z - 1]);
+    }
+  }
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int p = S.slack_rank[j];
+    unsigned long long ok = 0ULL;
+    int64_t acc = 0;
+    int c = 0;
+    for (int q = 0;; ++q) {
+      const int z = c + 1;
+      const double cs = div(mul(S.beta, i2d((int64_t)z * S.fi + S.far[j] + acc)), S.C);
+      const bool pass = !fails_margin(add(S.ws[j], cs), S.dl[j]) && !(S.has_cap && fails_margin(cs, S.cap_s));
+      if (pass) ok |= 1ULL << (z - 1);
+      else break;                        // the bound only grows with z
+      for (; q < n; ++q) {
+        const int i = S.far_order[q];
+        if (S.slack_rank[i] < p) break;
+      }
+      if (q >= n) break;
+      acc += S.far[S.far_order[q]];
+      ++c;
+    }
+    if (ok) atomicOr(&S.lat_ok, ok);
+  }
+  __syncthreads();
 }
 
 // Cooperative (block) load of one instance's members; returns after sync.
@@ -137,11 +190,8 @@ __device__ void load_members(Members& S, const Ctx& c, const eb_requests& req, i
     S.has_cap = c.has_cap;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    S.status = (s_err == INT_MAX) ? 0 : (s_err & 63);
-    build_level_bounds(S);
-  }
-  __syncthreads();
+  if (threadIdx.x == 0) S.status = (s_err == INT_MAX) ? 0 : (s_err & 63);
+  build_level_bounds(S);
 }
 
 // check_direct on the current combination given its prefix folds.
@@ -368,6 +418,20 @@ __global__ void __launch_bounds__(256) exh_range_kernel(const __grid_constant__ 
   }
 }
 
+// One block: the level bounds of one instance as a bit mask (bit z-1 = level
+// z not refuted).
+__global__ void __launch_bounds__(256) exh_levels_kernel(const __grid_constant__ RangeArgs A,
+                                                         unsigned long long* out) {
+  __shared__ Members S;
+  load_members(S, A.c, A.req, 0, A.n);
+  if (threadIdx.x != 0) return;
+  if (S.status) { *A.status = S.status; *out = 0ULL; return; }
+  unsigned long long m = 0ULL;
+  for (int z = 1; z <= A.n; ++z)
+    if (!level_infeasible(S, z)) m |= 1ULL << (z - 1);
+  *out = m;
+}
+
 }  // namespace
 
 int binom_init(cudaStream_t st) {
@@ -390,23 +454,32 @@ int launch_exh_batch(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, in
 }
 
 // One level of one instance over a rank range; synchronous; device pointers.
+static void fill_ctx(Ctx& c, const eb_context& ctx_host);
+
+// Live levels of one instance (synchronous; device pointers).
+int exh_levels(eb_handle* h, cudaStream_t st, const eb_context& ctx_host, const eb_requests& d_req, int n,
+               unsigned long long* d_mask, int* d_status, uint64_t* mask, int* status) {
+  RangeArgs A;
+  fill_ctx(A.c, ctx_host);
+  A.req = d_req; A.n = n; A.z = 0; A.lo = A.hi = 0; A.per = 1; A.best = d_mask; A.status = d_status;
+  int zero = 0;
+  EB_CUDA(cudaMemcpyAsync(d_status, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
+  exh_levels_kernel<<<1, 256, 0, st>>>(A, d_mask);
+  EB_CUDA(cudaGetLastError());
+  h->launches += 1;
+  unsigned long long m = 0;
+  EB_CUDA(cudaMemcpyAsync(&m, d_mask, sizeof(m), cudaMemcpyDeviceToHost, st));
+  EB_CUDA(cudaMemcpyAsync(status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  EB_CUDA(cudaStreamSynchronize(st));
+  *mask = m;
+  return EB_OK;
+}
+
 int exh_range(eb_handle* h, cudaStream_t st, const eb_context& ctx_host, const eb_requests& d_req,
               int n, int z, int64_t lo, int64_t hi, unsigned long long* d_best, int* d_status,
               int64_t* first_rank, int* status) {
   RangeArgs A;
-  // Ctx is built host-side with the same arithmetic (only products/sums of
-  // config scalars, no libm), mirroring load_ctx.
-  A.c.m.L = ctx_host.layers; A.c.m.d = ctx_host.hidden_dim; A.c.m.heads = ctx_host.head_count;
-  A.c.m.head_dim = ctx_host.head_dim; A.c.m.ffn = ctx_host.ffn_dim; A.c.m.bpp = ctx_host.bytes_per_param;
-  A.c.alpha = ctx_host.alpha; A.c.beta = ctx_host.beta; A.c.delta = ctx_host.delta_ppl;
-  A.c.B_up = ctx_host.uplink_band_hz; A.c.B_dn = ctx_host.downlink_band_hz; A.c.P_dn = ctx_host.downlink_power_w;
-  A.c.N0_up = ctx_host.noise_density_w_hz * ctx_host.uplink_band_hz;
-  A.c.N0_dn = ctx_host.noise_density_w_hz * ctx_host.downlink_band_hz;
-  A.c.T_up = ctx_host.uplink_slot_s; A.c.T_dn = ctx_host.downlink_slot_s;
-  A.c.fbits = (double)ctx_host.bits_per_token;
-  A.c.C = ctx_host.flops_per_s; A.c.M = ctx_host.memory_bytes; A.c.gpus = ctx_host.gpu_count;
-  A.c.has_cap = ctx_host.has_slot_cap != 0; A.c.cap_s = ctx_host.slot_cap_s;
-  A.c.slots = ctx_host.uplink_slot_s + ctx_host.downlink_slot_s;
+  fill_ctx(A.c, ctx_host);
   A.req = d_req; A.n = n; A.z = z; A.lo = lo; A.hi = hi;
   int64_t span = hi - lo;
   int threads = 256;
@@ -432,6 +505,24 @@ int exh_range(eb_handle* h, cudaStream_t st, const eb_context& ctx_host, const e
   EB_CUDA(cudaStreamSynchronize(st));
   *first_rank = (b == ULLONG_MAX) ? -1 : (int64_t)b;
   return EB_OK;
+}
+
+// Ctx is built host-side with the same arithmetic (only products/sums of
+// config scalars, no libm), mirroring load_ctx.
+static void fill_ctx(Ctx& c, const eb_context& ctx_host) {
+  RangeArgs A;
+  A.c.m.L = ctx_host.layers; A.c.m.d = ctx_host.hidden_dim; A.c.m.heads = ctx_host.head_count;
+  A.c.m.head_dim = ctx_host.head_dim; A.c.m.ffn = ctx_host.ffn_dim; A.c.m.bpp = ctx_host.bytes_per_param;
+  A.c.alpha = ctx_host.alpha; A.c.beta = ctx_host.beta; A.c.delta = ctx_host.delta_ppl;
+  A.c.B_up = ctx_host.uplink_band_hz; A.c.B_dn = ctx_host.downlink_band_hz; A.c.P_dn = ctx_host.downlink_power_w;
+  A.c.N0_up = ctx_host.noise_density_w_hz * ctx_host.uplink_band_hz;
+  A.c.N0_dn = ctx_host.noise_density_w_hz * ctx_host.downlink_band_hz;
+  A.c.T_up = ctx_host.uplink_slot_s; A.c.T_dn = ctx_host.downlink_slot_s;
+  A.c.fbits = (double)ctx_host.bits_per_token;
+  A.c.C = ctx_host.flops_per_s; A.c.M = ctx_host.memory_bytes; A.c.gpus = ctx_host.gpu_count;
+  A.c.has_cap = ctx_host.has_slot_cap != 0; A.c.cap_s = ctx_host.slot_cap_s;
+  A.c.slots = ctx_host.uplink_slot_s + ctx_host.downlink_slot_s;
+  c = A.c;
 }
 
 }  // namespace eb

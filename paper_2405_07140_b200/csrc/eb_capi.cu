@@ -41,6 +41,8 @@ int launch_exh_batch(eb_handle*, cudaStream_t, const eb_context*, int, int64_t, 
                      int64_t*, uint64_t*);
 int exh_range(eb_handle*, cudaStream_t, const eb_context&, const eb_requests&, int, int, int64_t, int64_t,
               unsigned long long*, int*, int64_t*, int*);
+int exh_levels(eb_handle*, cudaStream_t, const eb_context&, const eb_requests&, int, unsigned long long*, int*,
+               uint64_t*, int*);
 int launch_link(eb_handle*, cudaStream_t, const eb_context*, int, const eb_requests&, int64_t,
                 const int32_t*, int32_t*, double*);
 int launch_coeff(eb_handle*, cudaStream_t, const eb_context*, int, int64_t, const int64_t*, const int32_t*,
@@ -691,6 +693,25 @@ int32_t eb_exhaustive_level_range(eb_handle* h, const eb_context* ctx, int32_t k
   if (S.err) return S.err;
   int status = 0;
   int rc = exh_range(h, h->stream, *ctx, d_req, k, z, rank_lo, rank_hi, d_best, d_status, first_rank, &status);
+  if (rc) return rc;
+  rc = S.sync();
+  if (rc) return rc;
+  return status ? status : EB_OK;
+}
+
+int32_t eb_exhaustive_live_levels(eb_handle* h, const eb_context* ctx, int32_t k, const eb_requests* req,
+                                  uint64_t* live_mask) {
+  if (!h || !ctx || !req || !live_mask || k < 1 || k > EB_MAX_K || !req_complete(*req, false))
+    return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  *live_mask = 0;
+  Stage S(h, h->stream);
+  eb_requests d_req = upload_req(S, *req, 0, k);
+  unsigned long long* d_mask = S.alloc<unsigned long long>(1);
+  int* d_status = S.alloc<int>(1);
+  if (S.err) return S.err;
+  int status = 0;
+  int rc = exh_levels(h, h->stream, *ctx, d_req, k, d_mask, d_status, live_mask, &status);
   if (rc) return rc;
   rc = S.sync();
   if (rc) return rc;

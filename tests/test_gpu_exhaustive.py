@@ -98,3 +98,20 @@ def test_branch_and_bound_config2_pools():
         cols = {k: np.ascontiguousarray(v[lo:hi]) for k, v in b.columns.items()}
         got = solve_sharded(b.contexts[ci:ci + 1], cols, world=5)
         assert (got.z, got.lexrank, got.nodes_visited) == (int(z[i]), int(rk[i]), int(nodes[i])), i
+
+
+@pytest.mark.parametrize("seed", [31, 32])
+def test_live_levels_are_sound(seed):
+    """eb_exhaustive_live_levels never refutes a feasible level: every level
+    z <= z* (subsets of a feasible set are feasible) stays live."""
+    from paper_2405_07140_b200.brute import device_level_range
+    b, _ = random_batch(seed, 120, k_min=4, k_max=16, slot_cap_frac=0.6)
+    for i in range(b.n_inst):
+        ci = int(b.ctx_index[i])
+        lo, hi = int(b.offsets[i]), int(b.offsets[i + 1])
+        st, z, rk, nodes, mask = oracle.exhaustive(b.contexts[ci:ci + 1], b.columns, lo, hi)
+        if st != 0:
+            continue
+        cols = {k: np.ascontiguousarray(v[lo:hi]) for k, v in b.columns.items()}
+        live = device_level_range(b.contexts[ci:ci + 1], cols).live_mask
+        assert live & ((1 << z) - 1) == (1 << z) - 1, (i, z, bin(live))
