@@ -528,6 +528,23 @@ __global__ void count_table_kernel(const uint32_t* __restrict__ hdr, uint2* __re
   }
 }
 
+// Unranking prefix tables in closed form for partitions of at most three
+// levels: P_{k+1}[y] = #{count vectors of levels k+1 .. m-1 within their
+// class sizes, summing to at most y - 1} (P[0] = 0), the values build_pq
+// stores.  The last level admits one vector per sum up to its size; the
+// level above the last (m = 3) counts pairs (c1, c2) with c1 + c2 <= x:
+//   F(x) = (b + 1)(s2 + 1) + (a - b)(x + 1) - (a(a + 1) - b(b + 1)) / 2,
+//   a = min(s1, x), b = min(a, x - s2) (or -1 when x < s2).
+__device__ __forceinline__ uint32_t pq_closed(const LevelInfo* row, int m, int k, int y) {
+  if (y <= 0) return 0u;
+  const int x = y - 1;
+  if (k + 1 == m - 1) return (uint32_t)(min(x, (int)row[m - 1].size) + 1);
+  const int s1 = row[k + 1].size, s2 = row[k + 2].size;   // k + 1 == m - 2, m == 3
+  const int a = min(s1, x);
+  const int b = x - s2 >= 0 ? min(a, x - s2) : -1;
+  return (uint32_t)((b + 1) * (s2 + 1) + (a - b) * (x + 1) - (a * (a + 1) - b * (b + 1)) / 2);
+}
+
 template <bool PRUNE, bool INCL, bool EXACT, int NI>
 __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const Lay& L, const LevelInfo* lvl,
                           const uint8_t* ncls_d, const double* t_up, const double* t_dn, const double* t_tau,
@@ -659,7 +676,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       while (want) {
         const int dd = __ffsll((long long)want);
         want &= want - 1;
-        ok &= build_pq(dd);
+        if (ncls_d[dd - 1] >= 4) ok &= build_pq(dd);             // <= 3 levels: closed form (pq_closed)
         EB_STAT(5, 1);
         built |= 1ULL << (dd - 1);
       }
@@ -672,8 +689,11 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
         nall = (z <= row[0].size) ? 1u : 0u;
       } else {
         const uint32_t* P1 = pq + (size_t)(d - 1) * LV * W;        // level 1
+        const int m1 = ncls_d[d - 1];
         const int hi0 = min(z, (int)row[0].size), lo0 = max(0, z - (int)row[0].tail_next);
-        nall = (hi0 >= lo0) ? P1[z - lo0 + 1] - P1[z - hi0] : 0u;
+        if (hi0 < lo0) nall = 0u;
+        else if (m1 <= 3) nall = pq_closed(row, m1, 0, z - lo0 + 1) - pq_closed(row, m1, 0, z - hi0);
+        else nall = P1[z - lo0 + 1] - P1[z - hi0];
       }
       cnt = live ? nall : 0u;
     }
@@ -740,14 +760,15 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
             cc = r;
           } else {                                                 // unrank level k
             const uint32_t* P = base + (size_t)k * W;              // level k+1 prefix
+            auto Pv = [&](int y) -> uint32_t { return m <= 3 ? pq_closed(row, m, k, y) : P[y]; };
             const int hi = min(r, (int)li.size), lo = max(0, r - (int)li.tail_next);
-            const uint32_t pb = P[r - hi];
+            const uint32_t pb = Pv(r - hi);
             int xa = r - hi, xz = r - lo;
             while (xa < xz) {
               int mid = (xa + xz) >> 1;
-              if (P[mid + 1] - pb > i) xz = mid; else xa = mid + 1;
+              if (Pv(mid + 1) - pb > i) xz = mid; else xa = mid + 1;
             }
-            i -= P[xa] - pb;
+            i -= Pv(xa) - pb;
             cc = r - xa;
           }
           if (cc) { setV(V0, V1, k, cc); klast = k; }
