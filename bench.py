@@ -374,8 +374,9 @@ def main():
         e2e = {"value": world * n * args.steps / wire_s, "unit": "instances/s", "h2d_bytes_per_step": int(wb.nbytes()),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": wire_s / args.steps * 1e3,
                "path": "eb_dftsp_batch_packed(EB_MEM_HOST): pinned host buffers in the compact wire format "
-                       "(tokens u16, uniform uplink power, ids = row positions since they rise along every "
-                       "instance, uniform offsets), chunks n/64 doubling to n/16 on a 3-stream pipeline",
+                       "(token counts as one dictionary byte, uniform uplink power, ids = row positions since "
+                       "they rise along every instance, uniform offsets): 25 B/request; uploads on their own "
+                       "stream, chunks ramping n/64 -> n/16 -> n/64 over 3 compute streams",
                "wide": {"value": world * n * args.steps / wide_s, "h2d_bytes_per_step": int(h2d_wide),
                         "ms_per_step": wide_s / args.steps * 1e3, "path": "eb_dftsp_batch(EB_MEM_HOST), eb_requests"}}
 

@@ -184,9 +184,9 @@ int32_t eb_dftsp_batch(eb_handle *h, const eb_context *ctxs, int32_t n_ctx,
 /* ---- K3 over the compact wire format ------------------------------------
  * Same search and results as eb_dftsp_batch (dftsp.py:237-285), for host
  * callers whose request columns fit narrower types.  Fewer bytes cross
- * PCIe per request: 4 (id) + 2 + 2 (tokens) + 3 x 8 (deadline, waiting,
- * gain), plus 8 for uplink power unless it is uniform.  That is 32 B instead
- * of eb_requests' 48 B.  Each chunk is copied in this layout and widened on
+ * PCIe per request: 4 (id, or none) + 2 + 2 (tokens, or one dictionary
+ * byte) + 3 x 8 (deadline, waiting, gain), plus 8 for uplink power unless it
+ * is uniform.  That is 25-32 B instead of eb_requests' 48 B.  Each chunk is copied in this layout and widened on
  * the device by a copy kernel into eb_requests columns, so the search
  * reads exactly the values the wide call would.  Every narrowing is
  * lossless: Request.id (feasibility.py:35) and the token counts
@@ -206,7 +206,14 @@ typedef struct eb_requests_packed {
   const double *channel_gain;
   const double *uplink_power_w;   /* n_req values, or 1 if uplink_power_uniform */
   int32_t uplink_power_uniform;   /* 1: every request has uplink_power_w[0]     */
-  int32_t _pad;
+  /* Dictionary-coded token counts (when token_codes != NULL the two token
+   * columns are not read): code = prompt index | output index << 4 into the
+   * two value tables (at most 16 distinct values each), one byte per
+   * request instead of four. */
+  int32_t n_dict;                 /* 0, or the table length (<= 16) */
+  const uint8_t *token_codes;
+  int32_t prompt_dict[16];
+  int32_t output_dict[16];
 } eb_requests_packed;
 
 typedef struct eb_batch_packed {

@@ -77,7 +77,8 @@ class eb_batch(C.Structure):
 class eb_requests_packed(C.Structure):
     _fields_ = [("id", C.c_void_p), ("prompt_tokens", C.c_void_p), ("output_tokens", C.c_void_p),
                 ("deadline_s", C.c_void_p), ("waiting_s", C.c_void_p), ("channel_gain", C.c_void_p),
-                ("uplink_power_w", C.c_void_p), ("uplink_power_uniform", C.c_int32), ("_pad", C.c_int32)]
+                ("uplink_power_w", C.c_void_p), ("uplink_power_uniform", C.c_int32), ("n_dict", C.c_int32),
+                ("token_codes", C.c_void_p), ("prompt_dict", C.c_int32 * 16), ("output_dict", C.c_int32 * 16)]
 
 
 class eb_batch_packed(C.Structure):

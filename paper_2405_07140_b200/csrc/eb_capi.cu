@@ -154,15 +154,24 @@ eb_requests upload_req(Stage& S, const eb_requests& r, int64_t lo, int64_t n) {
 
 // Wire format -> eb_requests columns (lossless widening; uniform uplink
 // power broadcast).  deadline/waiting/gain are already f64 and stay in place.
+struct TokenDict { int32_t p[16], o[16]; };
+
 __global__ void widen_wire_kernel(int64_t nr, int64_t row0, const int32_t* __restrict__ id32,
                                   const uint16_t* __restrict__ p16, const uint16_t* __restrict__ o16,
+                                  const uint8_t* __restrict__ codes, const TokenDict dict,
                                   const double* __restrict__ pw, int uniform, int64_t* __restrict__ id64,
                                   int32_t* __restrict__ p32, int32_t* __restrict__ o32, double* __restrict__ pw64) {
   const double pw0 = uniform ? pw[0] : 0.0;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nr; j += (int64_t)gridDim.x * blockDim.x) {
     id64[j] = id32 ? (int64_t)id32[j] : row0 + j;      // NULL: ids are row positions
-    p32[j] = p16[j];
-    o32[j] = o16[j];
+    if (codes) {
+      const unsigned c = codes[j];
+      p32[j] = dict.p[c & 15u];
+      o32[j] = dict.o[c >> 4];
+    } else {
+      p32[j] = p16[j];
+      o32[j] = o16[j];
+    }
     pw64[j] = uniform ? pw0 : pw[j];
   }
 }
@@ -187,17 +196,24 @@ struct WideUp {
 struct WireStaged {
   const int32_t* id32;
   const uint16_t *p16, *o16;
+  const uint8_t* codes;
   const double *dl, *w, *g, *pw;
 };
 
 struct WireUp {
   const eb_requests_packed* r;
-  static size_t row_bytes() { return 4 + 2 + 2 + 8 + 8 + 8 + 8; }
+  static size_t row_bytes() { return 4 + 2 + 2 + 1 + 8 + 8 + 8 + 8; }
   WireStaged stage(Stage& S, int64_t lo, int64_t n) const {
     WireStaged d;
     d.id32 = r->id ? S.up(r->id + lo, n) : nullptr;
-    d.p16 = S.up(r->prompt_tokens + lo, n);
-    d.o16 = S.up(r->output_tokens + lo, n);
+    if (r->token_codes) {
+      d.codes = S.up(r->token_codes + lo, n);
+      d.p16 = d.o16 = nullptr;
+    } else {
+      d.codes = nullptr;
+      d.p16 = S.up(r->prompt_tokens + lo, n);
+      d.o16 = S.up(r->output_tokens + lo, n);
+    }
     d.dl = S.up(r->deadline_s + lo, n);
     d.w = S.up(r->waiting_s + lo, n);
     d.g = S.up(r->channel_gain + lo, n);
@@ -215,8 +231,10 @@ struct WireUp {
     int blocks = (int)((n + 255) / 256);
     if (blocks > 8 * S.h->num_sms) blocks = 8 * S.h->num_sms;
     if (blocks < 1) blocks = 1;
-    widen_wire_kernel<<<blocks, 256, 0, S.st>>>(n, lo, d.id32, d.p16, d.o16, d.pw, r->uplink_power_uniform != 0,
-                                                 id64, p32, o32, pw64);
+    TokenDict dict;
+    for (int q = 0; q < 16; ++q) { dict.p[q] = r->prompt_dict[q]; dict.o[q] = r->output_dict[q]; }
+    widen_wire_kernel<<<blocks, 256, 0, S.st>>>(n, lo, d.id32, d.p16, d.o16, d.codes, dict, d.pw,
+                                                 r->uplink_power_uniform != 0, id64, p32, o32, pw64);
     ++S.h->launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { S.err = cuda_fail(e, "widen_wire_kernel"); return q; }
@@ -585,9 +603,10 @@ int32_t eb_dftsp_batch_packed(eb_handle* h, const eb_context* ctxs, int32_t n_ct
     return EB_ERR_INVALID_ARG;
   if (prm->ladder_len < 0 || prm->ladder_len > EB_MAX_CLASSES) return EB_ERR_INVALID_ARG;
   const eb_requests_packed& r = b->req;
-  if (!r.prompt_tokens || !r.output_tokens || !r.deadline_s || !r.waiting_s || !r.channel_gain ||
-      !r.uplink_power_w)
+  if ((!r.token_codes && (!r.prompt_tokens || !r.output_tokens)) || !r.deadline_s || !r.waiting_s ||
+      !r.channel_gain || !r.uplink_power_w)
     return EB_ERR_INVALID_ARG;
+  if (r.token_codes && (r.n_dict < 1 || r.n_dict > 16)) return EB_ERR_INVALID_ARG;
   if (prm->collect_trajectory && (!out->traj || !out->traj_offsets)) return EB_ERR_INVALID_ARG;
   if (mem != EB_MEM_HOST) return EB_ERR_INVALID_ARG;
   if (b->k_max < 1 || b->k_max > EB_MAX_K) return EB_ERR_INVALID_ARG;

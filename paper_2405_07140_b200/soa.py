@@ -160,6 +160,11 @@ class WireBatch:
     ctx_index: object = None
     k_max: int = 0
     n_inst_: int = 0
+    # dictionary-coded token counts: token_codes (u8) = prompt index | output
+    # index << 4 into these tables (None: the u16 columns are shipped)
+    token_codes: np.ndarray | None = None
+    prompt_dict: np.ndarray | None = None
+    output_dict: np.ndarray | None = None
 
     @property
     def n_inst(self) -> int:
@@ -167,7 +172,7 @@ class WireBatch:
 
     @property
     def n_req(self) -> int:
-        return int(self.columns["prompt_tokens"].shape[0])
+        return int(self.columns["deadline_s"].shape[0])
 
     @property
     def uniform_power(self) -> bool:
@@ -181,6 +186,8 @@ class WireBatch:
     def nbytes(self) -> int:
         """Bytes one host->device pass of this batch moves."""
         n = sum(int(a.nbytes) for a in self.columns.values() if a is not None) + int(self.uplink_power_w.nbytes)
+        if self.token_codes is not None:
+            n += int(self.token_codes.nbytes)
         if self.offsets is not None:
             n += int(self.offsets.nbytes)
         if self.ctx_index is not None:
@@ -194,6 +201,13 @@ class WireBatch:
             setattr(r, name, ptr(a) if a is not None else None)
         r.uplink_power_w = ptr(self.uplink_power_w)
         r.uplink_power_uniform = int(self.uniform_power)
+        if self.token_codes is not None:
+            r.token_codes = ptr(self.token_codes)
+            r.n_dict = max(len(self.prompt_dict), len(self.output_dict))
+            for i, v in enumerate(self.prompt_dict):
+                r.prompt_dict[i] = int(v)
+            for i, v in enumerate(self.output_dict):
+                r.output_dict[i] = int(v)
         b = _lib.eb_batch_packed()
         b.n_inst = self.n_inst
         b.n_req = self.n_req
@@ -209,7 +223,9 @@ def pack_wire(batch: InstanceBatch, pin=None, implicit=True) -> WireBatch | None
     """The wire-format copy of a host batch, or None when a column does not
     narrow losslessly (ids outside int32, token counts outside uint16) or an
     instance is wider than EB_MAX_K.  With ``implicit``, ids that increase
-    along every instance's rows and uniform instance sizes are not shipped.
+    along every instance's rows and uniform instance sizes are not shipped,
+    and token counts with at most 16 distinct values each travel as one
+    dictionary byte per request.
     ``pin`` (e.g. ``lambda a: torch.from_numpy(a).pin_memory().numpy()``)
     places the arrays in pinned memory."""
     cols = batch.columns
@@ -221,6 +237,15 @@ def pack_wire(batch: InstanceBatch, pin=None, implicit=True) -> WireBatch | None
         if a.size and (a.min() < 0 or a.max() > 0xFFFF):
             return None
     out = {name: np.ascontiguousarray(cols[name], dtype=dt) for name, dt in WIRE_FIELDS if name != "id"}
+    codes = pdict = odict = None
+    if implicit and pt.size:
+        pdict, pcode = np.unique(pt, return_inverse=True)
+        odict, ocode = np.unique(ot, return_inverse=True)
+        if len(pdict) <= 16 and len(odict) <= 16:         # one dictionary byte per request
+            codes = (pcode.astype(np.uint8) | (ocode.astype(np.uint8) << 4)).astype(np.uint8)
+            out["prompt_tokens"] = out["output_tokens"] = None
+        else:
+            pdict = odict = None
     rising = False
     if implicit and ids.size:
         step = np.diff(ids) > 0
@@ -248,7 +273,8 @@ def pack_wire(batch: InstanceBatch, pin=None, implicit=True) -> WireBatch | None
         pw = pin(pw)
         off = None if off is None else pin(off)
         ci = None if ci is None else pin(ci)
-    return WireBatch(off, out, pw, batch.contexts, ci, k, batch.n_inst)
+        codes = None if codes is None else pin(codes)
+    return WireBatch(off, out, pw, batch.contexts, ci, k, batch.n_inst, codes, pdict, odict)
 
 
 def search_params(pruning=True, inclusive_bound=False, exact_tau=False, collect_trajectory=False, ladder=None,

@@ -131,6 +131,33 @@ def test_pack_wire_implicit_ids_and_offsets():
     assert pack_wire(InstanceBatch(batch.offsets, cols2, batch.contexts, batch.ctx_index, 7)).columns["id"] is not None
 
 
+def test_pack_wire_token_dictionary():
+    """Token counts with <= 16 distinct values travel as one code byte whose
+    tables decode every row exactly; more distinct values keep the u16 columns."""
+    import numpy as np
+    from paper_2405_07140_b200 import synth
+    from paper_2405_07140_b200.soa import pack_wire
+    rng = np.random.default_rng(0)
+    n = 500
+    from paper_2405_07140_b200.soa import REQ_FIELDS, InstanceBatch
+    cols = {name: np.zeros(n, dt) for name, dt in REQ_FIELDS}
+    cols["prompt_tokens"][:] = rng.choice([128, 256, 512], n)
+    cols["output_tokens"][:] = rng.choice([64, 128, 256, 512, 1024], n)
+    cols["id"][:] = np.tile(np.arange(20), n // 20)
+    cols["deadline_s"][:] = rng.uniform(0.5, 2, n)
+    off = np.arange(0, n + 1, 20, dtype=np.int64)
+    batch = InstanceBatch(off, cols, synth.contexts(synth.CONFIG2), np.zeros(n // 20, np.int32), 20)
+    w = pack_wire(batch)
+    assert w.token_codes is not None and w.columns["prompt_tokens"] is None
+    assert np.array_equal(w.prompt_dict[w.token_codes & 15], cols["prompt_tokens"])
+    assert np.array_equal(w.output_dict[w.token_codes >> 4], cols["output_tokens"])
+    s = w.struct()
+    assert s.req.n_dict == 5 and s.req.token_codes
+    cols["prompt_tokens"][:] = np.arange(n) % 40 + 1                  # 40 distinct prompts
+    w2 = pack_wire(InstanceBatch(off, cols, batch.contexts, batch.ctx_index, 20))
+    assert w2.token_codes is None and w2.columns["prompt_tokens"] is not None
+
+
 def test_no_gpu_means_loud_failure():
     """Without a device the product raises -- there is no CPU fallback."""
     import torch
