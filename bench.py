@@ -313,6 +313,11 @@ def main():
     # device results for accounting (and a parity spot check against the oracle)
     z = outs["z_found"].cpu().numpy()
     vis = outs["nodes_visited"].cpu().numpy()
+    sol = outs["solution"].cpu().numpy()
+    owner = np.repeat(np.arange(n), np.diff(batch.offsets))
+    bits = np.where(sol >= 0, np.left_shift(np.int64(1), np.maximum(sol, 0).astype(np.int64)), 0)
+    sol_mask = np.zeros(n, np.int64)
+    np.bitwise_or.at(sol_mask, owner, bits)
     status = outs["status"].cpu().numpy()
     assert (status == 0).all(), f"device statuses: {np.unique(status)}"
 
@@ -324,11 +329,14 @@ def main():
         def pinned(a):
             return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
 
+        # results a sweep consumes: status, z, node counts and the selected set
+        # (u64 mask per instance; the ids rise along the rows, so bit order is
+        # the solution's id order)
         hout = {"status": torch.zeros(n, dtype=torch.int32).pin_memory(),
                 "z_found": torch.zeros(n, dtype=torch.int32).pin_memory(),
                 "nodes_visited": torch.zeros(n, dtype=torch.int64).pin_memory(),
                 "nodes_pruned": torch.zeros(n, dtype=torch.int64).pin_memory(),
-                "solution": torch.zeros(nr, dtype=torch.int32).pin_memory()}
+                "solution_mask": torch.zeros(n, dtype=torch.int64).pin_memory()}
         hres = _lib.eb_dftsp_result()
         for k, t in hout.items():
             setattr(hres, k, t.data_ptr())
@@ -367,6 +375,7 @@ def main():
                 e1.synchronize()
                 et.append(e0.elapsed_time(e1) / 1e3)
             assert np.array_equal(hout["z_found"].numpy(), z) and np.array_equal(hout["nodes_visited"].numpy(), vis)
+            assert np.array_equal(hout["solution_mask"].numpy(), sol_mask)
             return max_over_ranks(sum(et), world, dev)
 
         wide_s = time_host(step_wide)

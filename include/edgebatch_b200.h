@@ -153,6 +153,12 @@ typedef struct eb_dftsp_result {
   const int64_t *traj_offsets; /* n_inst + 1 */
   int64_t *traj;             /* rows * 4 */
   int32_t *traj_len;         /* n_inst */
+  /* Optional: n_inst selection masks, bit j = local request j scheduled
+   * (instances of at most 64 requests; 0 for wider ones).  With ids that
+   * rise along the rows the mask's bit order is the solution's id order, so
+   * a caller can take it instead of `solution` (8 B per instance instead of
+   * 4 B per request). */
+  uint64_t *solution_mask;
 } eb_dftsp_result;
 
 typedef struct eb_handle eb_handle;

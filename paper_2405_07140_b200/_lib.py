@@ -98,7 +98,7 @@ class eb_dftsp_result(C.Structure):
                 ("nodes_visited", C.c_void_p), ("nodes_pruned", C.c_void_p), ("n_classes", C.c_void_p),
                 ("counts", C.c_void_p), ("class_lengths", C.c_void_p), ("solution", C.c_void_p),
                 ("metrics", C.c_void_p), ("traj_offsets", C.c_void_p), ("traj", C.c_void_p),
-                ("traj_len", C.c_void_p)]
+                ("traj_len", C.c_void_p), ("solution_mask", C.c_void_p)]
 
 
 P = C.c_void_p

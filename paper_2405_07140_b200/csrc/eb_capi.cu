@@ -398,6 +398,7 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
     d_out.class_lengths = S->out(out.class_lengths, ni * EB_MAX_CLASSES);
     d_out.solution = S->out(out.solution, nr);
     d_out.metrics = S->out(out.metrics, ni * EB_N_METRICS);
+    d_out.solution_mask = S->out(out.solution_mask, ni);
     int64_t T0 = 0;
     if (prm.collect_trajectory) {
       T0 = out.traj_offsets[i0];
@@ -421,6 +422,7 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
             ni * EB_MAX_CLASSES);
     S->down(out.solution ? out.solution + R0 : nullptr, d_out.solution, nr);
     S->down(out.metrics ? out.metrics + i0 * EB_N_METRICS : nullptr, d_out.metrics, ni * EB_N_METRICS);
+    S->down(out.solution_mask ? out.solution_mask + i0 : nullptr, d_out.solution_mask, ni);
     if (prm.collect_trajectory) {
       S->down(out.traj + 4 * T0, d_out.traj, (out.traj_offsets[i1] - T0) * 4);
       S->down(out.traj_len ? out.traj_len + i0 : nullptr, d_out.traj_len, ni);

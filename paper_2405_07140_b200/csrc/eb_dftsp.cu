@@ -1031,6 +1031,7 @@ __device__ __noinline__ void write_status(const eb_dftsp_result& O, int64_t inst
     O.nodes_pruned[inst] = 0;
     if (O.n_classes) O.n_classes[inst] = 0;
     if (O.traj_len) O.traj_len[inst] = 0;
+    if (O.solution_mask) O.solution_mask[inst] = 0ULL;
   }
   if (O.metrics && lane < EB_N_METRICS) O.metrics[inst * EB_N_METRICS + lane] = 0.0;
   if (lane < EB_MAX_CLASSES) {
@@ -1644,7 +1645,18 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
         O.solution[r0 + rank] = o_local[t];
       }
     }
+    if (status == EB_OK && O.solution_mask) {
+      uint64_t bits = 0;
+      for (int j = lane; j < zf; j += 32) {
+        const int loc = o_local[sol[j]];
+        if (loc < 64) bits |= 1ULL << loc;
+      }
+      bits = (uint64_t)__reduce_or_sync(EB_FULL, (unsigned)bits) |
+             ((uint64_t)__reduce_or_sync(EB_FULL, (unsigned)(bits >> 32)) << 32);
+      if (lane == 0) O.solution_mask[inst] = n <= 64 ? bits : 0ULL;
+    }
   }
+  if (O.solution_mask && lane == 0 && (!found || status != EB_OK)) O.solution_mask[inst] = 0ULL;
   // rows past the batch are unused: mark them
   if (O.solution)
     for (int j = lane; j < n; j += 32)

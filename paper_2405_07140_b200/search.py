@@ -191,6 +191,7 @@ class BatchResult:
     traj_offsets: np.ndarray | None = None
     traj: np.ndarray | None = None
     traj_len: np.ndarray | None = None
+    solution_mask: np.ndarray | None = None    # u64 per instance (K <= 64), bit j = local request j
 
 
 def solve_batch(batch: InstanceBatch | WireBatch, *, pruning=True, inclusive_bound=False, exact_tau=False,
@@ -207,10 +208,11 @@ def solve_batch(batch: InstanceBatch | WireBatch, *, pruning=True, inclusive_bou
                       nodes_pruned=np.zeros(n, np.int64), n_classes=np.zeros(n, np.int32),
                       counts=np.zeros((n, _lib.EB_MAX_CLASSES), np.int32),
                       class_lengths=np.zeros((n, _lib.EB_MAX_CLASSES), np.int32),
-                      solution=np.full(max(nr, 1), -1, np.int32), metrics=np.zeros((n, _lib.EB_N_METRICS)))
+                      solution=np.full(max(nr, 1), -1, np.int32), metrics=np.zeros((n, _lib.EB_N_METRICS)),
+                      solution_mask=np.zeros(max(n, 1), np.uint64))
     out = _lib.eb_dftsp_result()
     for name in ("status", "error_index", "z_found", "nodes_visited", "nodes_pruned", "n_classes", "counts",
-                 "class_lengths", "solution", "metrics"):
+                 "class_lengths", "solution", "metrics", "solution_mask"):
         setattr(out, name, getattr(res, name).ctypes.data)
     if collect_trajectory:
         rows = sizes * (sizes + 1) // 2

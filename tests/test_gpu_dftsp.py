@@ -269,7 +269,12 @@ def test_gpu_wire_format_implicit_ids_and_offsets():
     lad = (128, 256, 512)
     dev = search.solve_batch(b, ladder=lad)
     wire = search.solve_batch(w, ladder=lad)
-    for k in RES_KEYS + ("solution", "metrics", "error_index"):
+    for k in RES_KEYS + ("solution", "metrics", "error_index", "solution_mask"):
         assert np.array_equal(getattr(dev, k), getattr(wire, k)), k
     orc = oracle.dftsp_batch(b, ladder=lad, threads=8)
     _assert_same(wire, orc, b, "wire implicit")
+    # the selection mask names exactly the solution's local indices
+    for i in range(b.n_inst):
+        lo, z = int(b.offsets[i]), int(dev.z_found[i])
+        want = sum(1 << int(j) for j in dev.solution[lo:lo + z])
+        assert int(dev.solution_mask[i]) == want, i
