@@ -390,8 +390,11 @@ def main():
                         "ms_per_step": wide_s / args.steps * 1e3, "path": "eb_dftsp_batch(EB_MEM_HOST), eb_requests"}}
 
     # ---- roofline (rank 0 figures) + cpu baseline ---------------------------
+    # (no collectives below: the other ranks are done; rank 0 has the host)
+    if rank != 0:
+        return
     import oracle
-    sample = args.cpu_sample or 200_000
+    sample = args.cpu_sample or (200_000 if world == 1 else 50_000)
     threads = os.cpu_count() or 1
     cpu_rate, cpu_s, orc, sub = cpu_baseline(batch, min(sample, n), threads)
     parity_ok = bool(np.array_equal(orc["z_found"], z[:sub.n_inst]) and
