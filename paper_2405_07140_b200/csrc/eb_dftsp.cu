@@ -1959,29 +1959,47 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
     else kern = exact ? dftsp_lock_kernel<false, false, true, NI> : dftsp_lock_kernel<false, false, false, NI>; \
   }
   if (algo == 2) {
-    // lockstep blocks: up to 16 warps (one instance each) sharing phases
-    // (EB_LOCK_WARPS overrides the width, for tuning)
-    // Block width: the most resident warps per SM (shared memory: 228 KB
-    // per SM, 1 KB reserved per block; registers: 16 warps at 128 each),
-    // preferring wider blocks (measured at K=20: 4 -> 44.4, 8 -> 51.6,
-    // 16 -> 50.4 M inst/s).  Wide instances (K = 21..64) thus get e.g. two
-    // 5-warp blocks instead of one 8-warp block.
+    // Lockstep blocks (one instance per warp, phases shared by the block).
+    // Block width: the most resident warps per SM for this kernel's
+    // registers and this instance size's shared memory (occupancy API,
+    // cached per kernel and per-warp footprint), preferring wider blocks
+    // (measured at K=20: 4 -> 44.4, 8 -> 51.6, 16 -> 50.4 M inst/s).  Wide
+    // instances (K = 21..64) thus get e.g. two 5-warp blocks instead of one
+    // 8-warp block.  EB_LOCK_WARPS caps the width (tuning).
     int cap_w = 8;
     if (const char* e = getenv("EB_LOCK_WARPS")) { int v = atoi(e); if (v >= 1 && v <= 16) cap_w = v; }
+    if (K <= 32) { EB_PICKL3(1) } else { EB_PICKL3(2) }
     {
-      const size_t sm_bytes = 228 * 1024;
-      int best_w = 1, best_res = 0;
-      for (int w = 1; w <= cap_w; ++w) {
-        if (A.warp_bytes * w > smem_cap) break;
-        int blocks = (int)(sm_bytes / (A.warp_bytes * w + 1024));
-        if (blocks > 16 / w) blocks = 16 / w;
-        const int res = blocks * w;
-        if (res >= best_res) { best_res = res; best_w = w; }
+      struct WCache { void (*k)(DftspArgs); size_t wb; int cap; int dev; int w; };
+      static thread_local WCache wc[8];
+      static thread_local int nwc = 0;
+      int best_w = -1;
+      for (int i = 0; i < nwc && i < 8; ++i)
+        if (wc[i].k == kern && wc[i].wb == A.warp_bytes && wc[i].cap == cap_w && wc[i].dev == h->device) {
+          best_w = wc[i].w;
+          break;
+        }
+      if (best_w < 0) {
+        int best_res = 0;
+        best_w = 1;
+        for (int w = 1; w <= cap_w; ++w) {
+          const size_t sm = A.warp_bytes * w;
+          if (sm > smem_cap) break;
+          if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
+            cudaGetLastError();                 // beyond this kernel's limit: stop widening
+            break;
+          }
+          int blocks = 0;
+          EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * w, sm));
+          const int res = blocks * w;
+          if (res >= best_res) { best_res = res; best_w = w; }
+        }
+        wc[nwc % 8] = WCache{kern, A.warp_bytes, cap_w, h->device, best_w};
+        ++nwc;
       }
       warps = best_w;
     }
     smem = A.warp_bytes * warps;
-    if (K <= 32) { EB_PICKL3(1) } else { EB_PICKL3(2) }
   } else {
     EB_PICK(1)
   }
