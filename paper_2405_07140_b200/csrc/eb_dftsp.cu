@@ -1826,23 +1826,14 @@ extern "C" int eb_debug_stats(unsigned long long* out, int reset) {
 
 static int launch_one(eb_handle* h, cudaStream_t st, void (*kern)(DftspArgs), const DftspArgs& A, int warps,
                       size_t smem, int64_t n_inst) {
-  // occupancy per (kernel, block, smem) and the largest dynamic shared
-  // memory attribute set per kernel, cached per thread (the host pipeline
-  // launches every kernel once per chunk).  The attribute is a maximum, so
-  // it is only ever raised.
+  // occupancy per (kernel, block, smem), cached per thread (the host
+  // pipeline launches every kernel once per chunk).  The dynamic shared
+  // memory attribute is set on every launch: the block-width search of
+  // launch_dftsp moves it too.
   struct Occ { void (*k)(DftspArgs); int warps; size_t smem; int per_sm; int dev; };
-  struct Attr { void (*k)(DftspArgs); size_t smem; int dev; };
   static thread_local Occ occ[16];
-  static thread_local Attr attr[16];
-  static thread_local int nocc = 0, nattr = 0;
-  int ai = -1;
-  for (int i = 0; i < nattr && i < 16; ++i)
-    if (attr[i].k == kern && attr[i].dev == h->device) { ai = i; break; }
-  if (ai < 0 || attr[ai].smem < smem) {
-    EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (ai < 0) { ai = nattr % 16; ++nattr; }
-    attr[ai] = Attr{kern, smem, h->device};
-  }
+  static thread_local int nocc = 0;
+  EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = -1;
   for (int i = 0; i < nocc && i < 16; ++i)
     if (occ[i].k == kern && occ[i].warps == warps && occ[i].smem == smem && occ[i].dev == h->device) {
