@@ -162,7 +162,7 @@ def dfs(z, part, coeff, tau_min=None, *, pruning=True, inclusive_bound=False, ex
     h = _lib.handle()
     _lib.check(h.lib.eb_dfs_single(h.ptr, int(z), ncls, sizes.ctypes.data, lengths.ctypes.data, prompt.ctypes.data,
                                    k_up.ctypes.data, k_dn.ctypes.data, dl.ctypes.data, wt.ctypes.data,
-                                   int(coeff.padded_len), int(tau_min is not None),
+                                   co.ctypes.data, int(coeff.padded_len), int(tau_min is not None),
                                    float(tau_min) if tau_min is not None else 0.0, _ref(prm), ctypes.byref(found),
                                    counts.ctypes.data, ctypes.byref(vis), ctypes.byref(prn)),
                "eb_dfs_single")
