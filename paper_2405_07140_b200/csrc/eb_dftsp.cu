@@ -93,7 +93,8 @@ __host__ __device__ inline Lay make_lay(int K, int G, bool exact, bool v2) {
     // phase, after the search) share one region
     // the unranking tables (search), then the count rows of the lanes =
     // widths pass and the winner's count rows (counts phase) share a region
-    const size_t pq_bytes = 4 * (size_t)K * lvls * (K + 2), pf_bytes = 16 * (size_t)G * (K + 1);
+    // (partitions of at most three levels unrank in closed form: no tables)
+    const size_t pq_bytes = G >= 4 ? 4 * (size_t)K * lvls * (K + 2) : 0, pf_bytes = 16 * (size_t)G * (K + 1);
     const size_t rows_bytes = 32 * 2 * 4 * (size_t)(K + 1);
     size_t sc = pq_bytes > pf_bytes ? pq_bytes : pf_bytes;
     if (rows_bytes > sc) sc = rows_bytes;
@@ -122,6 +123,8 @@ struct DftspArgs {
   int64_t traj_base;          // absolute row of out.traj element 0
   int* counter;               // [0] instance queue, [1] fallback count
   const uint2* ctab;          // node-count table for this flag variant (K <= 64), or null
+  const int32_t* inst_list;   // wide pass: the instances to solve (indices), or null = all
+  const int* list_count;      // wide pass: length of inst_list (device)
   Lay lay;                    // per-warp shared-memory layout (make_lay(K, G, exact, algorithm 2))
   int fallback_pass;
 };
@@ -672,6 +675,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       uint64_t want = (uint64_t)__reduce_or_sync(EB_FULL, (unsigned)bit) |
                       ((uint64_t)__reduce_or_sync(EB_FULL, (unsigned)(bit >> 32)) << 32);
       want &= ~built;
+      if (Gi < 4) want = 0;                                     // <= 3 levels everywhere: closed form
       bool ok = true;
       while (want) {
         const int dd = __ffsll((long long)want);
@@ -872,7 +876,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       // running prefix; levels m-3 .. 1 in place over the u32 row (F(k, r)
       // reads PF_{k+1} only at indices <= r, so r descends, then a prefix).
       // Prefix sums are monotone, so checking the last one bounds the row.
-      if (ctab != nullptr && m <= 3 && !traj) {                     // tabulated shape: two lookups
+      if (ctab != nullptr && m <= 3 && d <= EB_MAX_K && !traj) {     // tabulated shape: two lookups
         const int lo = found ? (d > dwin ? zf + 1 : zf) : 1;
         if (lo <= d) {
           const uint32_t* hdr = (const uint32_t*)ctab;
@@ -1721,6 +1725,7 @@ __global__ void __launch_bounds__(32, 1) dftsp_wide_kernel(const __grid_constant
     if (inst >= A.n_inst) break;
     const int64_t n = A.offsets[inst + 1] - A.offsets[inst];
     if (n <= EB_MAX_K || n > EB_MAX_K_DFTSP) continue;
+    if (A.fallback_pass && A.out.status[inst] != EB_STATUS_FALLBACK) continue;   // after the v2 wide pass
     int passed = 0;
     solve_instance<PRUNE, INCL, EXACT, 1, (EB_MAX_K_DFTSP + 31) / 32>(A, inst, smem, passed);
     __syncwarp();
@@ -1729,28 +1734,53 @@ __global__ void __launch_bounds__(32, 1) dftsp_wide_kernel(const __grid_constant
 
 // Lockstep variant (leaf-parallel algorithm): the block takes one instance
 // per warp per round and all warps cross the same phase barriers.
-template <bool PRUNE, bool INCL, bool EXACT, int NI>
 #ifndef EB_LOCK_THREADS
 #define EB_LOCK_THREADS 512
 #endif
 #ifndef EB_LOCK_MINB
 #define EB_LOCK_MINB 1
 #endif
-__global__ void __launch_bounds__(EB_LOCK_THREADS, EB_LOCK_MINB) dftsp_lock_kernel(const __grid_constant__ DftspArgs A) {
+template <bool PRUNE, bool INCL, bool EXACT, int NI>
+__device__ __forceinline__ void lock_loop(const DftspArgs& A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   __shared__ int s_base;
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   unsigned char* smem = smem_all + warp * A.warp_bytes;
+  const int64_t total = A.list_count ? (int64_t)*A.list_count : A.n_inst;
   for (;;) {
     if (threadIdx.x == 0) s_base = atomicAdd(A.counter, nw);
     __syncthreads();
     const int64_t base = s_base;
-    if (base >= A.n_inst) break;
-    const int64_t inst = base + warp;
+    if (base >= total) break;
+    const int64_t slot = base + warp;
     int passed = 0;
-    if (inst < A.n_inst) solve_instance<PRUNE, INCL, EXACT, 2, NI>(A, inst, smem, passed);
+    if (slot < total)
+      solve_instance<PRUNE, INCL, EXACT, 2, NI>(A, A.inst_list ? (int64_t)A.inst_list[slot] : slot, smem, passed);
     __syncwarp();
     while (passed < 3) { __syncthreads(); ++passed; }
+  }
+}
+
+template <bool PRUNE, bool INCL, bool EXACT, int NI>
+__global__ void __launch_bounds__(EB_LOCK_THREADS, EB_LOCK_MINB) dftsp_lock_kernel(const __grid_constant__ DftspArgs A) {
+  lock_loop<PRUNE, INCL, EXACT, NI>(A);
+}
+
+// Wide instances (EB_MAX_K < n <= EB_MAX_K_DFTSP) with at most three classes
+// on the leaf-parallel search: up to 8 requests per lane, no unranking
+// tables (closed form), count rows past the table range; few warps per SM
+// (the per-warp footprint is O(K)), so the full register file per thread.
+template <bool PRUNE, bool INCL, bool EXACT>
+__global__ void __launch_bounds__(64, 1) dftsp_lock_wide_kernel(const __grid_constant__ DftspArgs A) {
+  lock_loop<PRUNE, INCL, EXACT, (EB_MAX_K_DFTSP + 31) / 32>(A);
+}
+
+// Indices of the instances wider than EB_MAX_K (order irrelevant).
+__global__ void wide_list_kernel(int64_t n, const int64_t* __restrict__ off, int32_t* __restrict__ list,
+                                 int* __restrict__ count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sz = off[i + 1] - off[i];
+    if (sz > EB_MAX_K && sz <= EB_MAX_K_DFTSP) list[atomicAdd(count, 1)] = (int32_t)i;
   }
 }
 
@@ -1856,12 +1886,15 @@ static int launch_one(eb_handle* h, cudaStream_t st, void (*kern)(DftspArgs), co
 }
 
 // Second pass over instances wider than EB_MAX_K (see dftsp_wide_kernel).
-static int launch_wide(eb_handle* h, cudaStream_t st, const DftspArgs& A0, int K_all, int64_t n_wide) {
+static int launch_wide(eb_handle* h, cudaStream_t st, const DftspArgs& A0, int K_all, int64_t n_wide,
+                       int fallback_only = 0) {
   DftspArgs W = A0;
   const int Kw = K_all < EB_MAX_K_DFTSP ? K_all : EB_MAX_K_DFTSP;
   W.K = Kw;
   W.G = A0.prm.ladder_len > 0 ? A0.prm.ladder_len : (Kw < EB_MAX_CLASSES ? Kw : EB_MAX_CLASSES);
-  W.fallback_pass = 0;
+  W.fallback_pass = fallback_only;
+  W.inst_list = nullptr;
+  W.list_count = nullptr;
   const bool exact = A0.prm.exact_tau != 0;
   W.lay = make_lay(Kw, W.G, exact, false);
   W.warp_bytes = al8(W.lay.total);
@@ -1895,6 +1928,61 @@ static int launch_wide(eb_handle* h, cudaStream_t st, const DftspArgs& A0, int K
   return EB_OK;
 }
 
+// Instances wider than EB_MAX_K: the leaf-parallel search when every
+// partition has at most three levels (ladder of <= 3 lengths) and the O(K)
+// per-warp footprint fits; the literal walk otherwise, and for any instance
+// whose u32 count rows overflow.
+static int launch_wide_v2(eb_handle* h, cudaStream_t st, const DftspArgs& A0, int K_all, int64_t n_wide) {
+  const int Kw = K_all < EB_MAX_K_DFTSP ? K_all : EB_MAX_K_DFTSP;
+  const int G = A0.prm.ladder_len > 0 ? A0.prm.ladder_len : (Kw < EB_MAX_CLASSES ? Kw : EB_MAX_CLASSES);
+  const bool exact = A0.prm.exact_tau != 0;
+  const size_t smem_cap = 227 * 1024;
+  const Lay lay = make_lay(Kw, G, exact, true);
+  if (G > 3 || al8(lay.total) > smem_cap || A0.prm.collect_trajectory) return launch_wide(h, st, A0, K_all, n_wide);
+  DftspArgs W = A0;
+  W.K = Kw;
+  W.G = G;
+  W.lay = lay;
+  W.warp_bytes = al8(lay.total);
+  W.fallback_pass = 0;
+  int* buf = nullptr;                                // [0] queue, [1] fallback count, [2] list count, list
+  EB_CUDA(cudaMallocAsync((void**)&buf, sizeof(int) * (4 + (size_t)W.n_inst), st));
+  EB_CUDA(cudaMemsetAsync(buf, 0, 4 * sizeof(int), st));
+  {
+    int blocks = (int)((W.n_inst + 255) / 256);
+    if (blocks > 4 * h->num_sms) blocks = 4 * h->num_sms;
+    if (blocks < 1) blocks = 1;
+    wide_list_kernel<<<blocks, 256, 0, st>>>(W.n_inst, W.offsets, buf + 4, buf + 2);
+    EB_CUDA(cudaGetLastError());
+    h->launches += 1;
+  }
+  W.counter = buf;
+  W.inst_list = buf + 4;
+  W.list_count = buf + 2;
+  void (*kern)(DftspArgs);
+  const bool P = W.prm.pruning != 0, I = W.prm.inclusive_bound != 0;
+  if (P) {
+    if (I) kern = exact ? dftsp_lock_wide_kernel<true, true, true> : dftsp_lock_wide_kernel<true, true, false>;
+    else kern = exact ? dftsp_lock_wide_kernel<true, false, true> : dftsp_lock_wide_kernel<true, false, false>;
+  } else {
+    if (I) kern = exact ? dftsp_lock_wide_kernel<false, true, true> : dftsp_lock_wide_kernel<false, true, false>;
+    else kern = exact ? dftsp_lock_wide_kernel<false, false, true> : dftsp_lock_wide_kernel<false, false, false>;
+  }
+  int warps = (int)(smem_cap / W.warp_bytes);
+  if (warps > 2) warps = 2;
+  const int64_t n_launch = n_wide > 0 ? n_wide : W.n_inst;        // grid bound only
+  int rc = launch_one(h, st, kern, W, warps, W.warp_bytes * warps, n_launch);
+  if (rc) return rc;
+  // literal walk for instances whose count rows overflowed (status flagged)
+  DftspArgs F = A0;
+  F.counter = buf;
+  EB_CUDA(cudaMemsetAsync(buf, 0, sizeof(int), st));
+  rc = launch_wide(h, st, F, K_all, n_wide, 1);
+  if (rc) return rc;
+  EB_CUDA(cudaFreeAsync(buf, st));
+  return EB_OK;
+}
+
 int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_ctx,
                  const eb_search_params& prm, int64_t n_inst, const int64_t* d_off,
                  const int32_t* d_ctx_index, int64_t req_base, const eb_requests& d_req,
@@ -1910,6 +1998,8 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   A.ctx_index = d_ctx_index; A.req_base = req_base; A.req = d_req; A.K = K; A.G = G;
   A.out = d_out; A.traj_base = traj_base; A.counter = d_counter; A.fallback_pass = 0;
   A.ctab = nullptr;
+  A.inst_list = nullptr;
+  A.list_count = nullptr;
   // algorithm: 2 = leaf-parallel (default) unless its tables do not fit two
   // warps per block, 1 = literal lanes-per-call (also v2's in-kernel fallback)
   int algo = prm.algorithm;
@@ -2040,7 +2130,7 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
       set_error("exhaustive counts mode supports at most %d candidates", EB_MAX_K);
       return EB_ERR_K_TOO_LARGE;
     }
-    return launch_wide(h, st, A, K_all, n_wide);
+    return launch_wide_v2(h, st, A, K_all, n_wide);
   }
   return EB_OK;
 }

@@ -214,7 +214,7 @@ def test_gpu_exhaustive_counts_mode_vs_oracle_fresh():
                 assert tuple(int(x) for x in res.solution[lo:lo + z]) == sol, j
 
 
-@pytest.mark.parametrize("tag", ["P", "PE", "PI", "NL"])
+@pytest.mark.parametrize("tag", ["P", "NP", "PE", "PI", "NL"])
 def test_gpu_wide_instances_mixed_with_narrow(tag):
     """Instances of 1..160 candidates in one call: the narrow ones take the
     main pass, those over 64 the wide pass; every field equals the oracle."""
@@ -229,6 +229,17 @@ def test_gpu_wide_instances_mixed_with_narrow(tag):
         dev = search.solve_batch(sb, ladder=lad, **flags)
         orc = oracle.dftsp_batch(sb, ladder=lad, threads=16, **flags)
         _assert_same(dev, orc, sb, f"mixed wide/narrow {tag} ladder {lad}")
+
+
+@pytest.mark.parametrize("tag", ["P", "NP"])
+def test_gpu_widest_instances(tag):
+    """Pools of 200..255 candidates (three classes): the leaf-parallel wide
+    pass, with count rows past the table range, equals the oracle."""
+    batch, ladders = random_batch(67, 12, k_min=200, k_max=255, max_classes=3)
+    for lad, (_, sb) in group_by_ladder(batch, ladders).items():
+        dev = search.solve_batch(sb, ladder=lad, **FLAGS[tag])
+        orc = oracle.dftsp_batch(sb, ladder=lad, threads=16, **FLAGS[tag])
+        _assert_same(dev, orc, sb, f"widest {tag} ladder {lad}")
 
 
 def test_gpu_over_wide_limit_is_k_too_large():

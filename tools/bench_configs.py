@@ -79,7 +79,7 @@ def device_rates(batch, ladder, reps=3):
     prm = search_params(ladder=ladder)
     ref = lambda x: ctypes.cast(ctypes.pointer(x), ctypes.c_void_p)  # noqa: E731
     wb = pack_wire(batch, pin=lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy())
-    wbs = wb.struct()
+    wbs = wb.struct() if wb is not None else None        # the wire format stops at EB_MAX_K
 
     def k_dev():
         _lib.check(h.lib.eb_dftsp_batch(h.ptr, d_ctx.data_ptr(), len(batch.contexts), ref(prm), ref(db), ref(dres),
@@ -102,7 +102,7 @@ def device_rates(batch, ladder, reps=3):
                 e1.synchronize()
                 best = min(best, e0.elapsed_time(e1) / 1e3)
         return n / best
-    return timed(k_dev), timed(k_wire)
+    return timed(k_dev), (timed(k_wire) if wbs is not None else float("nan"))
 
 
 def cpu_rate(batch, ladder, sample, threads):
