@@ -550,7 +550,7 @@ __device__ __forceinline__ uint32_t pq_closed(const LevelInfo* row, int m, int k
 
 template <bool PRUNE, bool INCL, bool EXACT, int NI>
 __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const Lay& L, const LevelInfo* lvl,
-                          const uint8_t* ncls_d, const double* t_up, const double* t_dn, const double* t_tau,
+                          const uint8_t* ncls_d,
                           const int32_t* c_len, const double* c_w, const double* o_tau, double k2, double k3,
                           double slot_base, bool has_cap, int padded, int64_t* traj, bool& found, int& zf,
                           int& dwin, int& kwin, uint64_t& W0, uint64_t& W1, int& best, uint64_t& tot_v,
@@ -1075,9 +1075,10 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   uint8_t* sizes = smem + L.sizes;
   uint8_t* ncls_d = smem + L.ncls;
   LevelInfo* lvl = (LevelInfo*)(smem + L.lvl);
-  double* t_up = (double*)(smem + L.t_up);
-  double* t_dn = (double*)(smem + L.t_dn);
-  double* t_tau = EXACT ? (double*)(smem + L.t_tau) : nullptr;
+  // per-width prefix tables: the literal walk only (v2 folds on the fly)
+  double* t_up = ALGO == 1 ? (double*)(smem + L.t_up) : nullptr;
+  double* t_dn = ALGO == 1 ? (double*)(smem + L.t_dn) : nullptr;
+  double* t_tau = (ALGO == 1 && EXACT) ? (double*)(smem + L.t_tau) : nullptr;
   uint64_t* ring_v = (uint64_t*)(smem + L.ring_v);
   uint64_t* ring_p = (uint64_t*)(smem + L.ring_p);
   uint8_t* ring_done = smem + L.ring_done;
@@ -1419,7 +1420,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   int zf = 0, dwin = 0, kwin = 0;
   uint64_t W0 = 0, W1 = 0;
   if constexpr (ALGO == 2) {
-    if (!search_v2<PRUNE, INCL, EXACT, NI>(passed, n, Gi, smem, L, lvl, ncls_d, t_up, t_dn, t_tau, c_len, c_w, o_tau, k2, k3,
+    if (!search_v2<PRUNE, INCL, EXACT, NI>(passed, n, Gi, smem, L, lvl, ncls_d, c_len, c_w, o_tau, k2, k3,
                                        slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
                                        tot_v, tot_p,
                                        CountsMode{A.prm.exhaustive_counts != 0, c_start, c_list, o_key, o_dnt},
