@@ -95,7 +95,8 @@ __host__ __device__ inline Lay make_lay(int K, int G, bool exact, bool v2) {
     // widths pass and the winner's count rows (counts phase) share a region
     // (partitions of at most three levels unrank in closed form: no tables)
     const size_t pq_bytes = G >= 4 ? 4 * (size_t)K * lvls * (K + 2) : 0, pf_bytes = 16 * (size_t)G * (K + 1);
-    const size_t rows_bytes = 32 * 2 * 4 * (size_t)(K + 1);
+    // (count rows only for partitions of four or more levels; three stream)
+    const size_t rows_bytes = G >= 4 ? 32 * 2 * 4 * (size_t)(K + 1) : 0;
     size_t sc = pq_bytes > pf_bytes ? pq_bytes : pf_bytes;
     if (rows_bytes > sc) sc = rows_bytes;
     L.pq = take(sc);
@@ -891,7 +892,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       const uint32_t sl = row[m - 1].size;
       auto pf_last = [&](int q, uint64_t& v, uint64_t& p) { last_level_prefix<PRUNE, INCL>(sl, (uint32_t)q, v, p); };
       auto pf_row = [&](int q, uint64_t& v, uint64_t& p) { v = RV[q]; p = RP[q]; };
-      if (m >= 3) {
+      if (m >= 4) {
         const LevelInfo li = row[m - 2];
         uint64_t av = 0, ap = 0;
         RV[0] = RP[0] = 0;
@@ -937,8 +938,35 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
           }
         }
       };
-      if (m >= 3) level0(pf_row);
-      else level0(pf_last);                                          // m == 2 (m == 1 never reads pf)
+      if (m >= 4) {
+        level0(pf_row);
+      } else if (m == 3) {
+        // Level 0 reads PF1 at r - xs and at r - xb - 1, two indices that
+        // never decrease with r: stream both prefix sums of F(1, .) (closed
+        // form against the last level) instead of storing a row, in u64.
+        // level_counts_f asks for the first, then the second, per r.
+        const LevelInfo l1 = row[1];
+        uint64_t va = 0, pa = 0, vb = 0, pb = 0;
+        int qa = 0, qb = 0;
+        bool second = false;
+        auto adv = [&](int q, int& qq, uint64_t& v, uint64_t& p) {
+          for (; qq < q;) {
+            ++qq;
+            uint64_t fv, fp;
+            level_counts_f<PRUNE, INCL>(l1, false, qq, pf_last, fv, fp);
+            v += fv;
+            p += fp;
+          }
+        };
+        auto pf_stream = [&](int q, uint64_t& v, uint64_t& p) {
+          if (!second) { adv(q, qa, va, pa); v = va; p = pa; }
+          else { adv(q, qb, vb, pb); v = vb; p = pb; }
+          second = !second;
+        };
+        level0(pf_stream);
+      } else {
+        level0(pf_last);                                             // m == 2 (m == 1 never reads pf)
+      }
     }
     if (__any_sync(EB_FULL, ovf)) return false;                    // exact literal-walk pass instead
     __syncwarp();
