@@ -1076,7 +1076,7 @@ __device__ __noinline__ void write_status(const eb_dftsp_result& O, int64_t inst
 
 template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI>
 __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* smem, int& passed,
-                               const int64_t* meta = nullptr) {
+                               bool have_meta = false, int64_t m_row0 = 0, int64_t m_row1 = 0, int m_ci = 0) {
   const int lane = threadIdx.x & 31;
   const int K = A.K, G = A.G;
   const Lay& L = A.lay;       // computed once on the host (make_lay)
@@ -1115,13 +1115,13 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   const eb_dftsp_result& O = A.out;
   // meta (lockstep kernel): offsets[inst], offsets[inst + 1] and the
   // context index, loaded a round ahead
-  const int64_t row0 = meta ? meta[0] : A.offsets[inst];
-  const int n = (int)((meta ? meta[1] : A.offsets[inst + 1]) - row0);
+  const int64_t row0 = have_meta ? m_row0 : A.offsets[inst];
+  const int n = (int)((have_meta ? m_row1 : A.offsets[inst + 1]) - row0);
   const int64_t r0 = row0 - A.req_base;
 
   auto put_status = [&](int st, int err) { write_status(O, inst, r0, n, st, err); };
 
-  int ci = meta ? (int)meta[2] : (A.ctx_index ? A.ctx_index[inst] : 0);
+  int ci = have_meta ? m_ci : (A.ctx_index ? A.ctx_index[inst] : 0);
   if (ci < 0 || ci >= A.n_ctx) { put_status(EB_ERR_INVALID_ARG, -1); return; }
   if (n == 0) { put_status(EB_OK, -1); return; }     // dftsp.py:253-254
   if (n > K || n > 32 * NI) { put_status(EB_ERR_K_TOO_LARGE, -1); return; }
@@ -1782,31 +1782,33 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
   auto inst_of = [&](int64_t slot) -> int64_t { return A.inst_list ? (int64_t)A.inst_list[slot] : slot; };
   // offsets / context index of a round's instance, loaded one round early so
   // the load latency hides behind the current round
-  auto meta_of = [&](int64_t slot, int64_t* m) {
+  // (scalars, so the loads stay in flight in registers until used)
+  auto meta_of = [&](int64_t slot, int64_t& r0, int64_t& r1, int& ci) {
     if (slot < total) {
       const int64_t i = inst_of(slot);
-      m[0] = A.offsets[i];
-      m[1] = A.offsets[i + 1];
-      m[2] = A.ctx_index ? A.ctx_index[i] : 0;
+      r0 = A.offsets[i];
+      r1 = A.offsets[i + 1];
+      ci = A.ctx_index ? A.ctx_index[i] : 0;
     }
   };
   if (threadIdx.x == 0) { s_q[0] = atomicAdd(A.counter, nw); s_q[1] = atomicAdd(A.counter, nw); }
   __syncthreads();
   int64_t base = s_q[0], nxt = s_q[1];
-  int64_t cur[3] = {0, 0, 0}, ahead[3] = {0, 0, 0};
-  meta_of(base + warp, cur);
+  int64_t c0 = 0, c1 = 0, a0 = 0, a1 = 0;
+  int cci = 0, aci = 0;
+  meta_of(base + warp, c0, c1, cci);
   for (int r = 0;; ++r) {
     if (base >= total) break;
     if (threadIdx.x == 0) s_q[(r + 2) % 3] = atomicAdd(A.counter, nw);   // read after this round's barriers
-    meta_of(nxt + warp, ahead);
+    meta_of(nxt + warp, a0, a1, aci);
     const int64_t slot = base + warp;
     int passed = 0;
-    if (slot < total) solve_instance<PRUNE, INCL, EXACT, 2, NI>(A, inst_of(slot), smem, passed, cur);
+    if (slot < total) solve_instance<PRUNE, INCL, EXACT, 2, NI>(A, inst_of(slot), smem, passed, true, c0, c1, cci);
     __syncwarp();
     while (passed < 3) { __syncthreads(); ++passed; }
     base = nxt;
     nxt = s_q[(r + 2) % 3];
-    cur[0] = ahead[0]; cur[1] = ahead[1]; cur[2] = ahead[2];
+    c0 = a0; c1 = a1; cci = aci;
   }
 }
 
