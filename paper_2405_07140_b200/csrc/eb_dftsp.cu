@@ -479,6 +479,16 @@ __host__ __device__ __forceinline__ int ct_row(const uint32_t* hdr, int m, int s
   return (int)hdr[CT * CT + CT] + s0 - 1;
 }
 
+// The same row index in closed form (no dependent header load on the
+// device): shapes are numbered s0-major with 64 - s0 - s1 rows per (s0, s1),
+// so the rows before s0 are Tet(62) - Tet(63 - s0), Tet(k) = k(k+1)(k+2)/6.
+__host__ __device__ __forceinline__ int ct_row_closed(int m, int s0, int s1, int s2) {
+  auto tet = [](int k) { return k * (k + 1) * (k + 2) / 6; };
+  if (m == 3) return tet(62) - tet(63 - s0) + (s1 - 1) * (64 - s0) - (s1 - 1) * s1 / 2 + s2 - 1;
+  if (m == 2) return 41664 + (s0 - 1) * 64 - (s0 - 1) * s0 / 2 + s1 - 1;
+  return 41664 + 2016 + s0 - 1;
+}
+
 // Host: the header (row offsets in shape order).
 static void ct_header(uint32_t* hdr) {
   for (int i = 0; i < CT_HDR; ++i) hdr[i] = 0;
@@ -880,9 +890,8 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       if (ctab != nullptr && m <= 3 && d <= EB_MAX_K && !traj) {     // tabulated shape: two lookups
         const int lo = found ? (d > dwin ? zf + 1 : zf) : 1;
         if (lo <= d) {
-          const uint32_t* hdr = (const uint32_t*)ctab;
           const uint2* T = (const uint2*)((const unsigned char*)ctab + CT_HDR_BYTES) +
-                           (size_t)ct_row(hdr, m, row[0].size, m > 1 ? row[1].size : 0, m > 2 ? row[2].size : 0) * CT;
+                           (size_t)ct_row_closed(m, row[0].size, m > 1 ? row[1].size : 0, m > 2 ? row[2].size : 0) * CT;
           const uint2 a = T[d], b = T[lo - 1];
           my_v += (uint64_t)(a.x - b.x) + (uint64_t)(d - lo + 1);    // + one root per call
           my_p += (uint64_t)(a.y - b.y);
@@ -2146,6 +2155,12 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
       EB_CUDA(cudaMalloc(&t, CT_HDR_BYTES + (size_t)CT_ROWS * CT * sizeof(uint2)));
       uint32_t hdr[CT_HDR];
       ct_header(hdr);
+      for (int s0 = 1; s0 <= 62; ++s0)                 // the device uses the closed form
+        for (int s1 = 1; s0 + s1 <= 63; ++s1)
+          if (ct_row(hdr, 3, s0, s1, 1) != ct_row_closed(3, s0, s1, 1)) {
+            set_error("count table numbering mismatch");
+            return EB_ERR_CUDA;
+          }
       EB_CUDA(cudaMemcpyAsync(t, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
       void (*bk)(const uint32_t*, uint2*) = !P ? count_table_kernel<false, false>
                                                : (I ? count_table_kernel<true, true> : count_table_kernel<true, false>);
