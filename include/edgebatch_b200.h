@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define EB_ABI_VERSION 1
+#define EB_ABI_VERSION 2   /* 2: wire format (eb_dftsp_batch_packed), solution masks */
 #define EB_MAX_K 64          /* candidates per instance (u64 subset masks)   */
 #define EB_MAX_K_DFTSP 255   /* dftsp instances: > EB_MAX_K take a wide pass   */
 #define EB_MAX_CLASSES 16    /* output-length classes per instance           */

@@ -15,6 +15,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libedgebatch_b200.so")
 
+ABI_VERSION = 2        # include/edgebatch_b200.h EB_ABI_VERSION
 EB_MAX_K = 64
 EB_MAX_CLASSES = 16
 EB_N_METRICS = 8
@@ -151,7 +152,7 @@ def load(path: str | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.eb_abi_version() != 1:
+        if lib.eb_abi_version() != ABI_VERSION:
             raise EdgebatchNativeError("ABI version mismatch")
         if path is None:
             _lib = lib

@@ -24,7 +24,7 @@ def test_library_builds_and_loads():
     path = build_library()
     assert os.path.exists(path)
     lib = _lib.load()
-    assert lib.eb_abi_version() == 1
+    assert lib.eb_abi_version() == _lib.ABI_VERSION == 2
     assert lib.eb_status_string(0) == b"ok"
 
 
