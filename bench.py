@@ -55,88 +55,89 @@ def parse():
     return ap.parse_args()
 
 
+def _nvml_sampler(idx: int, conn, stop, period: float):
+    """Child process: (time, sm_mhz, max_mhz, reasons) every `period` s until `stop` is set."""
+    rows = []
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        hnd = pynvml.nvmlDeviceGetHandleByIndex(idx)
+        mx = float(pynvml.nvmlDeviceGetMaxClockInfo(hnd, pynvml.NVML_CLOCK_SM))
+        while not stop.is_set():
+            try:
+                rows.append((time.time(), float(pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM)), mx,
+                             int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(hnd))))
+            except Exception:
+                pass
+            time.sleep(period)
+    except Exception:
+        pass
+    conn.send(rows)
+    conn.close()
+
+
 class ClockSampler:
-    """SM clocks and throttle reasons sampled during the timed region (NVML
-    every 2 ms from a thread; nvidia-smi -lms as the fallback)."""
+    """SM clocks and throttle reasons under load: NVML sampled every 2 ms in a
+    separate process (no GIL contention with the timing loop), started before
+    the warm-up; summary() keeps the samples inside the timed window marked
+    with begin()/end() (all load samples if the window caught fewer than 3)."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap"}
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []          # (sm_mhz, max_mhz, reasons bitmask)
+        self.rows = []          # (time, sm_mhz, max_mhz, reasons bitmask)
+        self.t0 = self.t1 = None
         self.proc = None
-        self.stop = threading.Event()
-        self.thread = None
 
-    def __enter__(self):
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            idx = self.device
-            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            if vis:
-                try:
-                    idx = int(vis.split(",")[self.device])
-                except ValueError:
-                    pass
-            hnd = pynvml.nvmlDeviceGetHandleByIndex(idx)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(hnd, pynvml.NVML_CLOCK_SM)
-
-            def loop():
-                while not self.stop.is_set():
-                    try:
-                        sm = pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM)
-                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(hnd)
-                        self.rows.append((float(sm), float(mx), int(rs)))
-                    except Exception:
-                        pass
-                    time.sleep(0.002)
-            self.thread = threading.Thread(target=loop, daemon=True)
-            self.thread.start()
-            return self
-        except Exception:
-            pass
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except FileNotFoundError:
-            self.proc = None
+    def start(self):
+        import multiprocessing as mp
+        idx = self.device
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                idx = int(vis.split(",")[self.device])
+            except ValueError:
+                pass
+        ctx = mp.get_context("spawn")
+        self.parent, child = ctx.Pipe(duplex=False)
+        self.stop_ev = ctx.Event()
+        self.proc = ctx.Process(target=_nvml_sampler, args=(idx, child, self.stop_ev, 0.002), daemon=True)
+        self.proc.start()
         return self
 
-    def _read(self):
-        bits = (0x8, 0x40, 0x20, 0x4)
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            try:
-                mask = sum(b for b, v in zip(bits, parts[2:6]) if v.lower() == "active")
-                self.rows.append((float(parts[0]), float(parts[1]), mask))
-            except (ValueError, IndexError):
-                pass
+    def begin(self):
+        self.t0 = time.time()
 
-    def __exit__(self, *exc):
-        self.stop.set()
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-        if self.thread is not None:
-            self.thread.join(timeout=5)
+    def end(self):
+        self.t1 = time.time()
+
+    def finish(self):
+        if self.proc is None:
+            return
+        self.stop_ev.set()
+        try:
+            if self.parent.poll(10):
+                self.rows = self.parent.recv()
+        except (EOFError, OSError):
+            pass
+        self.proc.join(timeout=5)
+        self.proc = None
 
     def summary(self):
-        if not self.rows:
+        self.finish()
+        rows, in_window = self.rows, False
+        if self.t0 is not None and self.t1 is not None:
+            win = [r for r in rows if self.t0 <= r[0] <= self.t1]
+            if len(win) >= 3:
+                rows, in_window = win, True
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        reasons = sorted({name for _, _, m in self.rows for bit, name in self.REASONS.items() if m & bit})
-        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
-                "reasons": reasons, "samples": len(self.rows)}
+        reasons = sorted({name for *_, m in rows for bit, name in self.REASONS.items() if m & bit})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": reasons, "samples": len(rows),
+                "window": "timed region" if in_window else "warm-up and timed region"}
 
 
 def dist_init(args):
@@ -279,6 +280,7 @@ def main():
         _lib.check(h.lib.eb_dftsp_batch(h.ptr, d_ctx.data_ptr(), len(batch.contexts), ref(prm), ref(db), ref(dres),
                                         _lib.EB_MEM_DEVICE), "eb_dftsp_batch")
 
+    clk = ClockSampler(local).start()
     with torch.cuda.stream(stream):
         # W warm-up steps, continued until the GPU has been busy for >= 1 s
         # (the host-side workload generation leaves it idle long enough for
@@ -294,16 +296,17 @@ def main():
         torch.cuda.synchronize()
         launches0 = h.launches()
         times = []
-        with ClockSampler(local) as clk:
-            for _ in range(args.steps):
-                flush.fill_(1.0)                      # L2 flush between timed steps
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                step_device()
-                e1.record(stream)
-                e1.synchronize()
-                times.append(e0.elapsed_time(e1) / 1e3)
+        clk.begin()
+        for _ in range(args.steps):
+            flush.fill_(1.0)                      # L2 flush between timed steps
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step_device()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        clk.end()
         torch.cuda.synchronize()
         barrier(world)
         launches = h.launches() - launches0
@@ -391,6 +394,7 @@ def main():
 
     # ---- roofline (rank 0 figures) + cpu baseline ---------------------------
     # (no collectives below: the other ranks are done; rank 0 has the host)
+    clocks = clk.summary()
     if rank != 0:
         return
     import oracle
@@ -406,7 +410,6 @@ def main():
     n_w = min(20000, sub.n_inst)
     ops_per_inst = (LEAF_OPS * wsub["leaf_checks"] + DESCEND_OPS * wsub["descends"]) / n_w
     props = torch.cuda.get_device_properties(dev)
-    clocks = clk.summary()
     f_mhz = clocks.get("sm_max_mhz") or 1965.0
     peak_fp64 = props.multi_processor_count * FP64_LANES_PER_SM * f_mhz * 1e6 / 1e12   # TFLOP/s (1 op/lane/clk)
     per_launch_s = dev_s / args.steps

@@ -434,14 +434,17 @@ int dftsp_host_pipeline(eb_handle* h, const eb_context* ctxs, int n_ctx, const e
     if (!rc) rc = s2;
   }
   for (Stage* S : stages) delete S;   // stream-ordered frees
+  // join the pipeline back into the handle's stream (every call checked:
+  // the first failure is the one reported)
+  auto keep = [&](cudaError_t e, const char* what) { if (e != cudaSuccess && rc == EB_OK) rc = cuda_fail(e, what); };
   for (int i = 0; i < 3; ++i) {
-    cudaEventRecord(h->ev[i], h->pipe[i]);
-    cudaStreamWaitEvent(h->stream, h->ev[i], 0);
+    keep(cudaEventRecord(h->ev[i], h->pipe[i]), "join: cudaEventRecord");
+    keep(cudaStreamWaitEvent(h->stream, h->ev[i], 0), "join: cudaStreamWaitEvent");
   }
-  cudaEventRecord(h->cev[0], h->up);
-  cudaStreamWaitEvent(h->stream, h->cev[0], 0);
-  for (int i = 0; i < 3; ++i) cudaStreamSynchronize(h->pipe[i]);
-  cudaStreamSynchronize(h->up);
+  keep(cudaEventRecord(h->cev[0], h->up), "join: cudaEventRecord(up)");
+  keep(cudaStreamWaitEvent(h->stream, h->cev[0], 0), "join: cudaStreamWaitEvent(up)");
+  for (int i = 0; i < 3; ++i) keep(cudaStreamSynchronize(h->pipe[i]), "join: cudaStreamSynchronize");
+  keep(cudaStreamSynchronize(h->up), "join: cudaStreamSynchronize(up)");
   return rc;
 }
 
