@@ -398,7 +398,7 @@ def main():
     if rank != 0:
         return
     import oracle
-    sample = args.cpu_sample or (200_000 if world == 1 else 50_000)
+    sample = args.cpu_sample or (n if world == 1 else 50_000)     # N=1: the whole 10^6-instance workload
     threads = os.cpu_count() or 1
     cpu_rate, cpu_s, orc, sub = cpu_baseline(batch, min(sample, n), threads)
     parity_ok = bool(np.array_equal(orc["z_found"], z[:sub.n_inst]) and
@@ -464,7 +464,7 @@ def run_reference(args, world, rank):
         batch_src = "device-admitted synthetic workload"
     except Exception:
         batch_src = None
-    sample = args.cpu_sample or 100_000
+    sample = args.cpu_sample or 1_000_000                        # the same 10^6 instances per step
     batch = synth.generate(synth.CONFIG2, sample, seed=2405_07140)
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
