@@ -464,7 +464,9 @@ def run_reference(args, world, rank):
         batch_src = "device-admitted synthetic workload"
     except Exception:
         batch_src = None
-    sample = args.cpu_sample or 1_000_000                        # the same 10^6 instances per step
+    # up to the same 10^6 instances per step, bounded so that the whole
+    # warm-up + timed run stays near a minute (~2.6e5 inst/s on 16 threads)
+    sample = args.cpu_sample or min(1_000_000, max(50_000, int(15e6 / max(1, args.steps + args.warmup))))
     batch = synth.generate(synth.CONFIG2, sample, seed=2405_07140)
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
