@@ -205,8 +205,18 @@ def issue_roofline(sms: int, f_mhz: float, n: int, per_launch_s: float):
         return None
     achieved = wi * n / per_launch_s / 1e9
     peak = sms * 4 * f_mhz * 1e6 / 1e9
-    return {"achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "G warp-inst/s",
-            "frac": round(achieved / peak, 4), "warp_inst_per_instance_ncu": wi}
+    out = {"achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "G warp-inst/s",
+           "frac": round(achieved / peak, 4), "warp_inst_per_instance_ncu": wi}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_dftsp_summary.json")) as fh:
+            j = json.load(fh)
+        # warp-execution efficiency (active lanes per issued warp instruction / 32)
+        # and the scenario-array stream rate, from the same capture
+        out["warp_execution_efficiency_ncu"] = round(j["threads_per_warp_inst"] / 32.0, 4)
+        out["hbm_gb_s_ncu"] = round(j["dram_bytes_per_launch"] / (j["duration_ms"] * 1e-3) / 1e9, 1)
+    except (OSError, ValueError, KeyError, TypeError, ZeroDivisionError):
+        pass
+    return out
 
 
 def cpu_baseline(batch, sample: int, threads: int):
