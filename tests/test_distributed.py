@@ -119,3 +119,33 @@ def test_instance_sharding_gloo_world2():
     b, _ = random_batch(44, 64, k_max=10, max_classes=1)
     full = oracle.dftsp_batch(b, ladder=None)
     assert res[0] == res[1] == [int(full["nodes_visited"].sum()), int(full["z_found"].sum())]
+
+
+def _bench_timing_worker(rank, world, port, q):
+    """bench.py's multi-rank plumbing on gloo: the max-over-ranks timing
+    reduction and the barrier (NCCL on the GPU box; same calls)."""
+    import sys
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    bench.barrier(world)
+    t = bench.max_over_ranks(0.25 + rank, world)          # each rank's elapsed seconds
+    q.put((rank, t))
+    dist.destroy_process_group()
+
+
+def test_bench_max_over_ranks_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_timing_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert got == {0: 1.25, 1: 1.25}          # every rank reports the slowest rank's time
