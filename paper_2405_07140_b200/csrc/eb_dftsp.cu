@@ -1,25 +1,30 @@
 // eb_dftsp.cu -- K3: instance-parallel DFTSP (reference dftsp.py:237-285).
 //
-// One warp per scheduling instance (persistent warps pull instances from an
-// atomic queue).  Inside the warp:
+// One warp per scheduling instance.  Inside the warp:
 //   setup   lanes = requests: coefficients (feasibility.py:133-167, device
 //           glibc-log2 port), normalized-deadline order (dftsp.py:257),
 //           output-length classes and within-class uplink order
-//           (dftsp.py:54-82), then lanes = (d, class) pairs build every
-//           pool-width-d prefix table (SearchTables.build dftsp.py:110-132)
-//           in shared memory;
-//   search  lanes = dfs calls.  The reference walks calls (z from K down, d
-//           from z up) until the first success; here the 32 lanes run 32
-//           consecutive calls of that sequence concurrently, each lane a
-//           literal restatement of the dfs node loop (dftsp.py:153-234)
-//           with its accumulators in registers (recomputed on backtrack
-//           from the packed count stack, bit-identically).  Lanes pull the
-//           next call when they finish; a warp ballot/min keeps the first
-//           successful call in sequence order, aborts speculative calls
-//           behind it, and folds node counts in sequence order -- so
-//           nodes_visited / nodes_pruned equal the reference's totals.
+//           (dftsp.py:54-82), class sizes per pool width (ballots).
+//   search  two algorithms with identical results.
+//           v2 (leaf-parallel, default; search_v2): windows of 32 dfs calls
+//           (lane = call) of the reference's (z, d) sequence after a
+//           per-target skip; sound greedy-leaf skip per call; the surviving
+//           calls' leaves unranked and checked 32 at a time (class prefixes
+//           folded on the fly exactly as SearchTables.build sums them);
+//           node counts from the combinatorial recurrence F(k, r) -- a
+//           per-handle table for <= 64 requests and <= 3 classes, streamed
+//           or row-based otherwise -- plus the winner's partial count.
+//           v1 (literal; dfs_step): lanes = consecutive dfs calls, each a
+//           restatement of the dfs node loop (dftsp.py:153-234); the v2
+//           fallback (u32 count overflow) and the path for >= 4 classes
+//           above 64 requests.
 //   finish  recover_subset + check_direct re-verification (dftsp.py:276),
-//           solution sorted by id, derived metrics.
+//           solution sorted by id (and as a selection mask), derived metrics.
+// Kernels: dftsp_lock_kernel (v2, lockstep blocks: every warp of a block
+// crosses the same phase barriers, so an SM runs one phase's code at a time),
+// dftsp_lock_wide_kernel (v2, 65..255 requests, <= 3 classes), dftsp_kernel
+// (v1 main/fallback pass), dftsp_wide_kernel (v1, 65..255 requests),
+// count_table_kernel (node-count tables), dfs_single_kernel (one dfs call).
 #include <climits>
 #include <cstdlib>
 
