@@ -1646,13 +1646,17 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       pb = max(pb, o_s[t]);
       fl_pool += flops_autoregressive(C.m, padded, o_len[t]);
     }
-    pb = __reduce_max_sync(EB_FULL, pb);
-    for (int j = lane; j < zf; j += 32) fl_batch += flops_autoregressive(C.m, pb, o_len[sol[j]]);
+    // the batch-padding cost (sim.py:372-376) only feeds the optional metrics
+    const bool want_met = O.metrics != nullptr;
+    if (want_met) {
+      pb = __reduce_max_sync(EB_FULL, pb);
+      for (int j = lane; j < zf; j += 32) fl_batch += flops_autoregressive(C.m, pb, o_len[sol[j]]);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       sn += __shfl_xor_sync(EB_FULL, sn, o);
       fl_pool += __shfl_xor_sync(EB_FULL, fl_pool, o);
-      fl_batch += __shfl_xor_sync(EB_FULL, fl_batch, o);
+      if (want_met) fl_batch += __shfl_xor_sync(EB_FULL, fl_batch, o);
     }
     fl_pool += (int64_t)zf * fi_pad;                                   // z * flops_initial + sum(...)
     const double compute_s = compute_seconds(C, fl_pool);
@@ -1672,16 +1676,18 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       if (ok && C.has_cap) ok = leq(compute_s, C.cap_s);
       if (ok && late) ok = false;
       if (!ok) status = EB_ERR_REVERIFY;
-      // batch_cost at the batch's own padding (sim.py:372-376)
-      int64_t mem_b = m1 + kv * (int64_t)pb * zf + kv * sn;
-      fl_batch += (int64_t)zf * flops_initial(C.m, pb);
-      met[EB_MET_UP_SUM] = up;
-      met[EB_MET_DN_SUM] = dn;
-      met[EB_MET_MEM_POOLPAD] = mul(C.alpha, i2d(mem));
-      met[EB_MET_LAT_POOLPAD] = compute_s;
-      met[EB_MET_MEM_BATCHPAD] = mul(C.alpha, i2d(mem_b));
-      met[EB_MET_LAT_BATCHPAD] = compute_seconds(C, fl_batch);
-      met[EB_MET_WIN_D] = (double)dwin;
+      if (want_met) {
+        // batch_cost at the batch's own padding (sim.py:372-376)
+        int64_t mem_b = m1 + kv * (int64_t)pb * zf + kv * sn;
+        fl_batch += (int64_t)zf * flops_initial(C.m, pb);
+        met[EB_MET_UP_SUM] = up;
+        met[EB_MET_DN_SUM] = dn;
+        met[EB_MET_MEM_POOLPAD] = mul(C.alpha, i2d(mem));
+        met[EB_MET_LAT_POOLPAD] = compute_s;
+        met[EB_MET_MEM_BATCHPAD] = mul(C.alpha, i2d(mem_b));
+        met[EB_MET_LAT_BATCHPAD] = compute_seconds(C, fl_batch);
+        met[EB_MET_WIN_D] = (double)dwin;
+      }
     }
     status = __shfl_sync(EB_FULL, status, 0);
     __syncwarp();
