@@ -396,9 +396,14 @@ __device__ __forceinline__ void level_counts(const LevelInfo& li, bool last, int
 // Phase barrier of the lockstep (ALGO 2) kernel: every warp of the block
 // passes the same three barriers per instance round, so the SM executes one
 // phase's code at a time (instruction-cache locality).
+#ifndef EB_LOCK_BARRIERS
+#define EB_LOCK_BARRIERS 3   // which phase barriers synchronize (bit i = barrier i; measured: 3 > 5 > 7 > 1)
+#endif
 template <int ALGO>
 __device__ __forceinline__ void phase_barrier(int& passed) {
-  if constexpr (ALGO == 2) __syncthreads();
+  if constexpr (ALGO == 2) {
+    if ((EB_LOCK_BARRIERS >> passed) & 1) __syncthreads();
+  }
   ++passed;
 }
 
@@ -1825,7 +1830,8 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
     int passed = 0;
     if (slot < total) solve_instance<PRUNE, INCL, EXACT, 2, NI>(A, inst_of(slot), smem, passed, true, c0, c1, cci);
     __syncwarp();
-    while (passed < 3) { __syncthreads(); ++passed; }
+    for (; passed < 3; ++passed)
+      if ((EB_LOCK_BARRIERS >> passed) & 1) __syncthreads();
     base = nxt;
     nxt = s_q[(r + 2) % 3];
     c0 = a0; c1 = a1; cci = aci;
