@@ -636,6 +636,17 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
   // z's (tau descends with d).  If it fails width z's caps by the margin, no
   // call (z, d) can contain a passing leaf, so the call sequence starts at
   // the largest z that survives (lanes = z).  Counts mode needs every call.
+  // Exact per-leaf tau (dftsp.py:128): a leaf's tau is the least of its z
+  // members' deadlines among the first d by tau, so it is at most the z-th
+  // largest, o_tau[z - 1]; min(o_tau[z - 1] - k3 z, slot_budget(z)) thus
+  // bounds every leaf cap of target z from above, for every width.  (With a
+  // NaN deadline the tau ranks are not a permutation: slot budget only.)
+  bool tau_ok = true;
+  if (EXACT) {
+    bool nan = false;
+    for (int t = lane; t < n; t += 32) nan |= !(o_tau[t] == o_tau[t]);
+    tau_ok = !__any_sync(EB_FULL, nan);
+  }
   int c_first = 0;
   if (!cm.on) {
     const LevelInfo* rown = lvl + (size_t)(n - 1) * Gi;
@@ -655,7 +666,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
         lat = add(lat, mul(i2d(cc), c_w[li.g]));
         rem -= cc;
       }
-      const double lat_cap = EXACT ? slot_cap : pymin(sub(o_tau[z - 1], k3z), slot_cap);
+      const double lat_cap = (EXACT && !tau_ok) ? slot_cap : pymin(sub(o_tau[z - 1], k3z), slot_cap);
       if (!(fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap)))
         zhi = z;
     }
@@ -685,7 +696,8 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
         lat = add(lat, mul(i2d(cc), c_w[li.g]));
         rem -= cc;
       }
-      const double lat_cap = EXACT ? slot_cap : pymin(sub(o_tau[d - 1], k3z), slot_cap);
+      const double lat_cap = EXACT ? (tau_ok ? pymin(sub(o_tau[z - 1], k3z), slot_cap) : slot_cap)
+                                   : pymin(sub(o_tau[d - 1], k3z), slot_cap);
       live = !(fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap));
     }
     // unranking tables for surviving widths (once per width); counts mode
