@@ -699,6 +699,33 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       const double lat_cap = EXACT ? (tau_ok ? pymin(sub(o_tau[z - 1], k3z), slot_cap) : slot_cap)
                                    : pymin(sub(o_tau[d - 1], k3z), slot_cap);
       live = !(fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap));
+      if (EXACT && tau_ok && live && !cm.on) {
+        // Exact tau: a member t whose own deadline fails the greedy latency
+        // (o_tau[t] - k3 z < lat by the margin) is in no passing leaf, so a
+        // passing leaf takes at most lim_k of class k (its members before the
+        // first such one, in key order among the first d).  The greedy fill of
+        // that box bounds every in-box leaf's memory and latency from below.
+        const double lat_m = mul(lat, 0.999999999999);
+        int r2 = z;
+        int64_t mem2 = 0;
+        double lat2 = 0.0;
+        for (int k = 0; k < m && r2 > 0; ++k) {
+          const LevelInfo li = row[k];
+          int lim = 0;
+          for (int p = cm.c_start[li.g], seen = 0; seen < (int)li.size && lim < r2; ++p) {
+            const int t = cm.c_list[p];
+            if (t >= d) continue;
+            ++seen;
+            if (fails_with_margin(lat_m, sub(o_tau[t], k3z))) break;
+            ++lim;
+          }
+          mem2 += (int64_t)lim * c_len[li.g];
+          lat2 = add(lat2, mul(i2d(lim), c_w[li.g]));
+          r2 -= lim;
+        }
+        live = r2 == 0 && !(fails_with_margin(i2d(mem2), mem_cap) ||
+                            fails_with_margin(mul(lat2, 0.999999999999), lat_cap));
+      }
     }
     // unranking tables for surviving widths (once per width); counts mode
     // needs every call's vector count, skipped or not
