@@ -4,7 +4,7 @@ build with -DEB_STATS; not the product library).  Builds
 build/stats/libedgebatch_b200.so, runs N config-2 instances and prints per
 instance: windows, windows with live leaves, leaf batches, leaves, U-table
 builds, live calls, calls in sequence up to the winner.
-  python tools/search_stats.py [--build-only] [--exact] [N]"""
+  python tools/search_stats.py [--build-only] [--exact] [--config5] [N]"""
 import ctypes
 import os
 import subprocess
@@ -34,10 +34,11 @@ def main():
     _lib.LIB_PATH = OUT
     lib = _lib.load()
     lib.eb_debug_stats.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    b = synth.generate(synth.CONFIG2, n, seed=5)
+    w = synth.CONFIG5 if "--config5" in sys.argv else synth.CONFIG2
+    b = synth.generate(w, n, seed=5)
     st = (ctypes.c_ulonglong * 16)()
     lib.eb_debug_stats(st, 1)
-    res = search.solve_batch(b, ladder=(128, 256, 512), exact_tau="--exact" in sys.argv)
+    res = search.solve_batch(b, ladder=tuple(w.outputs), exact_tau="--exact" in sys.argv)
     lib.eb_debug_stats(st, 0)
     names = ["instances", "windows", "windows_T>0", "leaf_batches", "leaves", "u_builds", "live_calls",
              "calls_to_winner"]
