@@ -531,6 +531,7 @@ int32_t eb_handle_destroy(eb_handle* h) {
   if (h->pinned) cudaFreeHost(h->pinned);
   for (int i = 0; i < 3; ++i) {
     if (h->ctab[i]) cudaFree(h->ctab[i]);
+    if (h->ctab_m[i]) cudaFree(h->ctab_m[i]);
     if (h->arena[i]) cudaFree(h->arena[i]);
   }
   delete h;

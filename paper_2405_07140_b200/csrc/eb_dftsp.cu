@@ -129,6 +129,7 @@ struct DftspArgs {
   int64_t traj_base;          // absolute row of out.traj element 0
   int* counter;               // [0] instance queue, [1] fallback count
   const uint2* ctab;          // node-count table for this flag variant (K <= 64), or null
+  const uint2* ctab_m;        // four/five-class node-count table (widths <= CTM_K), or null
   const int32_t* inst_list;   // wide pass: the instances to solve (indices), or null = all
   const int* list_count;      // wide pass: length of inst_list (device)
   Lay lay;                    // per-warp shared-memory layout (make_lay(K, G, exact, algorithm 2))
@@ -552,6 +553,84 @@ __global__ void count_table_kernel(const uint32_t* __restrict__ hdr, uint2* __re
   }
 }
 
+// Node-count tables for four and five output classes at pool widths up to
+// CTM_K (the config-5 shape): per partition shape s0..s_{m-1} >= 1 with
+// sum d <= CTM_K, a row of PF0(q), q = 0..CTM_K, as in count_table_kernel.
+// Shapes are numbered by the colex rank of their partial sums
+// t_i = s_0 + .. + s_i (1 <= t_0 < .. < t_{m-1} = d <= CTM_K):
+// rank = sum_i C(t_i - 1, i + 1), m = 4 rows first.  237,336 rows, 62.7 MB
+// per flag variant.  Without them each width runs the level recurrence over
+// a u32 row on its own lane (one lane per width, work ~ m d, lanes idle).
+constexpr int CTM_K = 32;
+constexpr int CTM = CTM_K + 1;
+constexpr int CTM_ROWS4 = 35960;                          // C(32, 4)
+constexpr int CTM_ROWS = CTM_ROWS4 + 201376;              // + C(32, 5)
+
+__host__ __device__ __forceinline__ int binom_small(int a, int k) {
+  int r = 1;
+  for (int j = 0; j < k; ++j) r = r * (a - j) / (j + 1);  // C(a, j + 1), exact at every step
+  return r;
+}
+
+__host__ __device__ __forceinline__ int ctm_row(int m, const int* sz) {
+  int t = 0, rank = m == 5 ? CTM_ROWS4 : 0;
+  for (int i = 0; i < m; ++i) { t += sz[i]; rank += binom_small(t - 1, i + 1); }
+  return rank;
+}
+
+template <bool PRUNE, bool INCL>
+__global__ void count_table_m_kernel(uint2* __restrict__ rows) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n4 = 32LL * 32 * 32 * 32, n5 = n4 * 32;
+  int m, sz[5];
+  int64_t u;
+  if (t < n4) { m = 4; u = t; } else if (t < n4 + n5) { m = 5; u = t - n4; } else return;
+  int d = 0;
+  for (int i = m - 1; i >= 0; --i) { sz[i] = 1 + (int)(u & 31); u >>= 5; d += sz[i]; }
+  if (d > CTM_K) return;
+  LevelInfo row[5];
+  int tail = 0;
+  for (int k = m - 1; k >= 0; --k) {
+    row[k].off = 0; row[k].size = (uint8_t)sz[k]; row[k].tail_next = (uint8_t)tail; row[k].g = (uint8_t)k;
+    row[k].pad[0] = row[k].pad[1] = row[k].pad[2] = 0;
+    tail += sz[k];
+  }
+  const uint32_t sl = sz[m - 1];
+  auto pf_last = [&](int q, uint64_t& v, uint64_t& p) { last_level_prefix<PRUNE, INCL>(sl, (uint32_t)q, v, p); };
+  uint32_t RV[CTM] = {}, RP[CTM] = {};
+  auto pf_row = [&](int q, uint64_t& v, uint64_t& p) { v = RV[q]; p = RP[q]; };
+  {                                   // level m-2 against the closed-form last level, prefix-summed
+    uint64_t av = 0, ap = 0;
+    for (int r = 1; r <= d; ++r) {
+      uint64_t fv, fp;
+      level_counts_f<PRUNE, INCL>(row[m - 2], false, r, pf_last, fv, fp);
+      av += fv; ap += fp;
+      RV[r] = (uint32_t)av; RP[r] = (uint32_t)ap;
+    }
+  }
+  for (int k = m - 3; k >= 1; --k) {  // in place: F(k, r) reads PF_{k+1} at indices <= r
+    for (int r = d; r >= 1; --r) {
+      uint64_t fv, fp;
+      level_counts_f<PRUNE, INCL>(row[k], false, r, pf_row, fv, fp);
+      RV[r] = (uint32_t)fv; RP[r] = (uint32_t)fp;
+    }
+    uint64_t bv = 0, bp = 0;
+    for (int r = 1; r <= d; ++r) {
+      bv += RV[r]; bp += RP[r];
+      RV[r] = (uint32_t)bv; RP[r] = (uint32_t)bp;
+    }
+  }
+  uint2* out = rows + (size_t)ctm_row(m, sz) * CTM;
+  uint64_t av = 0, ap = 0;
+  out[0] = make_uint2(0u, 0u);
+  for (int r = 1; r <= d; ++r) {      // (< 2^32: at most C(37, 5) nodes per call, 32 calls)
+    uint64_t fv, fp;
+    level_counts_f<PRUNE, INCL>(row[0], false, r, pf_row, fv, fp);
+    av += fv; ap += fp;
+    out[r] = make_uint2((uint32_t)av, (uint32_t)ap);
+  }
+}
+
 // Unranking prefix tables in closed form for partitions of at most three
 // levels: P_{k+1}[y] = #{count vectors of levels k+1 .. m-1 within their
 // class sizes, summing to at most y - 1} (P[0] = 0), the values build_pq
@@ -575,7 +654,8 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
                           const int32_t* c_len, const double* c_w, const double* o_tau, double k2, double k3,
                           double slot_base, bool has_cap, int padded, int64_t* traj, bool& found, int& zf,
                           int& dwin, int& kwin, uint64_t& W0, uint64_t& W1, int& best, uint64_t& tot_v,
-                          uint64_t& tot_p, const CountsMode& cm, const uint2* ctab, const uint8_t* sizes) {
+                          uint64_t& tot_p, const CountsMode& cm, const uint2* ctab, const uint2* ctab_m,
+                          const uint8_t* sizes) {
   const int lane = threadIdx.x & 31;
   uint64_t cm_before = 0;   // counts mode: count vectors tried in completed windows
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
@@ -943,6 +1023,18 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
                            (size_t)ct_row_closed(m, row[0].size, m > 1 ? row[1].size : 0, m > 2 ? row[2].size : 0) * CT;
           const uint2 a = T[d], b = T[lo - 1];
           my_v += (uint64_t)(a.x - b.x) + (uint64_t)(d - lo + 1);    // + one root per call
+          my_p += (uint64_t)(a.y - b.y);
+        }
+        continue;
+      }
+      if (ctab_m != nullptr && (m == 4 || m == 5) && d <= CTM_K && !traj) {  // four/five classes
+        const int lo = found ? (d > dwin ? zf + 1 : zf) : 1;
+        if (lo <= d) {
+          int sz[5];
+          for (int k = 0; k < m; ++k) sz[k] = row[k].size;
+          const uint2* T = ctab_m + (size_t)ctm_row(m, sz) * CTM;
+          const uint2 a = T[d], b = T[lo - 1];
+          my_v += (uint64_t)(a.x - b.x) + (uint64_t)(d - lo + 1);
           my_p += (uint64_t)(a.y - b.y);
         }
         continue;
@@ -1510,7 +1602,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
                                        slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
                                        tot_v, tot_p,
                                        CountsMode{A.prm.exhaustive_counts != 0, c_start, c_list, o_key, o_dnt},
-                                       A.ctab, sizes)) {
+                                       A.ctab, A.ctab_m, sizes)) {
       // leaf counts overflow the u32 unranking tables: hand the instance to
       // the literal walk (second pass of launch_dftsp)
       put_status(EB_STATUS_FALLBACK, -1);
@@ -2114,6 +2206,7 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   A.ctx_index = d_ctx_index; A.req_base = req_base; A.req = d_req; A.K = K; A.G = G;
   A.out = d_out; A.traj_base = traj_base; A.counter = d_counter; A.fallback_pass = 0;
   A.ctab = nullptr;
+  A.ctab_m = nullptr;
   A.inst_list = nullptr;
   A.list_count = nullptr;
   // algorithm: 2 = leaf-parallel (default) unless its tables do not fit two
@@ -2228,6 +2321,21 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
       h->ctab[v] = t;
     }
     A.ctab = (const uint2*)h->ctab[v];
+    if (G >= 4) {
+      if (!h->ctab_m[v]) {
+        void* t = nullptr;
+        EB_CUDA(cudaMalloc(&t, (size_t)CTM_ROWS * CTM * sizeof(uint2)));
+        void (*bk)(uint2*) = !P ? count_table_m_kernel<false, false>
+                                : (I ? count_table_m_kernel<true, true> : count_table_m_kernel<true, false>);
+        const int64_t nthr = 32LL * 32 * 32 * 32 * 33;
+        bk<<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>((uint2*)t);
+        EB_CUDA(cudaGetLastError());
+        h->launches += 1;
+        EB_CUDA(cudaStreamSynchronize(st));
+        h->ctab_m[v] = t;
+      }
+      A.ctab_m = (const uint2*)h->ctab_m[v];
+    }
   }
   EB_CUDA(cudaMemsetAsync(d_counter, 0, 2 * sizeof(int), st));
   int rc = launch_one(h, st, kern, A, warps, smem, n_inst);

@@ -92,6 +92,7 @@ struct eb_handle {
   // (0: pruning off, 1: pruning, 2: pruning + inclusive bound); built on
   // first use (eb_dftsp.cu count_table_kernel)
   void* ctab[3];
+  void* ctab_m[3];     // four/five-class tables (eb_dftsp.cu count_table_m_kernel)
   // per pipeline stream device arena of the host-memory DFTSP path (grow-only;
   // chunk c and chunk c+3 share a stream, so reuse is stream-ordered)
   void* arena[3];
