@@ -566,15 +566,23 @@ constexpr int CTM = CTM_K + 1;
 constexpr int CTM_ROWS4 = 35960;                          // C(32, 4)
 constexpr int CTM_ROWS = CTM_ROWS4 + 201376;              // + C(32, 5)
 
+// C(a, k) for 0 <= a < CTM_K, k = 1..5 (0 when a < k: the product has a zero
+// factor); constant divisors
 __host__ __device__ __forceinline__ int binom_small(int a, int k) {
-  int r = 1;
-  for (int j = 0; j < k; ++j) r = r * (a - j) / (j + 1);  // C(a, j + 1), exact at every step
-  return r;
+  switch (k) {
+    case 1: return a;
+    case 2: return a * (a - 1) / 2;
+    case 3: return a * (a - 1) * (a - 2) / 6;
+    case 4: return a * (a - 1) * (a - 2) * (a - 3) / 24;
+    default: return a * (a - 1) * (a - 2) * (a - 3) * (a - 4) / 120;
+  }
 }
 
 __host__ __device__ __forceinline__ int ctm_row(int m, const int* sz) {
   int t = 0, rank = m == 5 ? CTM_ROWS4 : 0;
-  for (int i = 0; i < m; ++i) { t += sz[i]; rank += binom_small(t - 1, i + 1); }
+#pragma unroll
+  for (int i = 0; i < 5; ++i)
+    if (i < m) { t += sz[i]; rank += binom_small(t - 1, i + 1); }
   return rank;
 }
 
@@ -676,21 +684,18 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
     if (m < 2) return true;
     const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
     uint32_t* base = pq + (size_t)(d - 1) * LV * W;
-    {
-      uint32_t* P = base + (size_t)(m - 2) * W;         // level m-1: Q(r) = [r <= s]
-      const int sl = row[m - 1].size;
-      for (int x = lane; x <= n + 1; x += 32) P[x] = (x == 0) ? 0u : (uint32_t)(min(x - 1, sl) + 1);
-    }
-    __syncwarp();
+    // levels m-1 and m-2 are closed forms (pq_closed); tables for m-3 .. 1
     bool ovf = false;
-    for (int k = m - 2; k >= 1; --k) {
+    for (int k = m - 3; k >= 1; --k) {
       const uint32_t* Pn = base + (size_t)k * W;        // level k+1
       uint32_t* Pk = base + (size_t)(k - 1) * W;        // level k
       const int sk = row[k].size;
+      const bool closed = k + 1 >= m - 2;
       bool o2 = false;
       warp_prefix1<NI + 1>(n,
           [&](int r) -> uint64_t {
             int lo = r - sk - 1;
+            if (closed) return (uint64_t)pq_closed(row, m, k, r + 1) - (lo >= 0 ? (uint64_t)pq_closed(row, m, k, lo + 1) : 0);
             return (uint64_t)Pn[r + 1] - (lo >= 0 ? (uint64_t)Pn[lo + 1] : 0);
           },
           [&](int r, uint64_t a) {
@@ -904,7 +909,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
             cc = r;
           } else {                                                 // unrank level k
             const uint32_t* P = base + (size_t)k * W;              // level k+1 prefix
-            auto Pv = [&](int y) -> uint32_t { return m <= 3 ? pq_closed(row, m, k, y) : P[y]; };
+            auto Pv = [&](int y) -> uint32_t { return (m <= 3 || k + 1 >= m - 2) ? pq_closed(row, m, k, y) : P[y]; };
             const int hi = min(r, (int)li.size), lo = max(0, r - (int)li.tail_next);
             const uint32_t pb = Pv(r - hi);
             int xa = r - hi, xz = r - lo;

@@ -30,7 +30,7 @@ def _same(dev, orc, batch, what):
 
 
 @pytest.mark.parametrize("tag", ["P", "NP", "PI", "PE"])
-@pytest.mark.parametrize("shape", [(1, 32, 3, 24000), (33, 64, 3, 4800), (4, 24, 5, 6000), (65, 120, 3, 600)])
+@pytest.mark.parametrize("shape", [(1, 32, 3, 24000), (33, 64, 3, 4800), (4, 24, 5, 6000), (20, 64, 5, 1500), (65, 120, 3, 600)])
 def test_stress_against_oracle(tag, shape):
     k_min, k_max, max_classes, n = shape
     seed = 7000 + 97 * k_min + 13 * max_classes + sum(map(ord, tag))
