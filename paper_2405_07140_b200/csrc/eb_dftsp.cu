@@ -129,7 +129,6 @@ struct DftspArgs {
   int64_t traj_base;          // absolute row of out.traj element 0
   int* counter;               // [0] instance queue, [1] fallback count
   const uint2* ctab;          // node-count table for this flag variant (K <= 64), or null
-  const uint2* ctab_m;        // four/five-class node-count table (widths <= CTM_K), or null
   const int32_t* inst_list;   // wide pass: the instances to solve (indices), or null = all
   const int* list_count;      // wide pass: length of inst_list (device)
   Lay lay;                    // per-warp shared-memory layout (make_lay(K, G, exact, algorithm 2))
@@ -483,6 +482,9 @@ constexpr int CT = 65;
 constexpr int CT_HDR = CT * CT + CT + 1;                  // u32 entries
 constexpr size_t CT_HDR_BYTES = ((size_t)CT_HDR * 4 + 255) & ~(size_t)255;
 constexpr int CT_ROWS = 41664 + 2016 + 64;                // C(64,3) + C(64,2) + 64
+// the header's spare tail holds the four/five-class table's address (or 0)
+constexpr size_t CT_MPTR_OFF = ((size_t)CT_HDR * 4 + 7) & ~(size_t)7;
+static_assert(CT_MPTR_OFF + 8 <= CT_HDR_BYTES, "count-table header has no room for the pointer");
 
 __host__ __device__ __forceinline__ int ct_row(const uint32_t* hdr, int m, int s0, int s1, int s2) {
   if (m == 3) return (int)hdr[s0 * CT + s1] + s2 - 1;
@@ -662,8 +664,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
                           const int32_t* c_len, const double* c_w, const double* o_tau, double k2, double k3,
                           double slot_base, bool has_cap, int padded, int64_t* traj, bool& found, int& zf,
                           int& dwin, int& kwin, uint64_t& W0, uint64_t& W1, int& best, uint64_t& tot_v,
-                          uint64_t& tot_p, const CountsMode& cm, const uint2* ctab, const uint2* ctab_m,
-                          const uint8_t* sizes) {
+                          uint64_t& tot_p, const CountsMode& cm, const uint2* ctab, const uint8_t* sizes) {
   const int lane = threadIdx.x & 31;
   uint64_t cm_before = 0;   // counts mode: count vectors tried in completed windows
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
@@ -909,7 +910,8 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
             cc = r;
           } else {                                                 // unrank level k
             const uint32_t* P = base + (size_t)k * W;              // level k+1 prefix
-            auto Pv = [&](int y) -> uint32_t { return (m <= 3 || k + 1 >= m - 2) ? pq_closed(row, m, k, y) : P[y]; };
+            // closed form for the last two levels (every level when m <= 3)
+            auto Pv = [&](int y) -> uint32_t { return k >= m - 3 ? pq_closed(row, m, k, y) : P[y]; };
             const int hi = min(r, (int)li.size), lo = max(0, r - (int)li.tail_next);
             const uint32_t pb = Pv(r - hi);
             int xa = r - hi, xz = r - lo;
@@ -1032,12 +1034,16 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
         }
         continue;
       }
-      if (ctab_m != nullptr && (m == 4 || m == 5) && d <= CTM_K && !traj) {  // four/five classes
+      const uint2* ctab_m = (ctab != nullptr && (m == 4 || m == 5) && d <= CTM_K && !traj)
+                                ? *(const uint2* const*)((const unsigned char*)ctab + CT_MPTR_OFF) : nullptr;
+      if (ctab_m != nullptr) {                                        // four/five classes
         const int lo = found ? (d > dwin ? zf + 1 : zf) : 1;
         if (lo <= d) {
-          int sz[5];
-          for (int k = 0; k < m; ++k) sz[k] = row[k].size;
-          const uint2* T = ctab_m + (size_t)ctm_row(m, sz) * CTM;
+          int t = 0, rank = m == 5 ? CTM_ROWS4 : 0;                  // ctm_row, sizes from the row
+#pragma unroll
+          for (int i = 0; i < 5; ++i)
+            if (i < m) { t += row[i].size; rank += binom_small(t - 1, i + 1); }
+          const uint2* T = ctab_m + (size_t)rank * CTM;
           const uint2 a = T[d], b = T[lo - 1];
           my_v += (uint64_t)(a.x - b.x) + (uint64_t)(d - lo + 1);
           my_p += (uint64_t)(a.y - b.y);
@@ -1607,7 +1613,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
                                        slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
                                        tot_v, tot_p,
                                        CountsMode{A.prm.exhaustive_counts != 0, c_start, c_list, o_key, o_dnt},
-                                       A.ctab, A.ctab_m, sizes)) {
+                                       A.ctab, sizes)) {
       // leaf counts overflow the u32 unranking tables: hand the instance to
       // the literal walk (second pass of launch_dftsp)
       put_status(EB_STATUS_FALLBACK, -1);
@@ -2211,7 +2217,6 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   A.ctx_index = d_ctx_index; A.req_base = req_base; A.req = d_req; A.K = K; A.G = G;
   A.out = d_out; A.traj_base = traj_base; A.counter = d_counter; A.fallback_pass = 0;
   A.ctab = nullptr;
-  A.ctab_m = nullptr;
   A.inst_list = nullptr;
   A.list_count = nullptr;
   // algorithm: 2 = leaf-parallel (default) unless its tables do not fit two
@@ -2316,6 +2321,7 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
             return EB_ERR_CUDA;
           }
       EB_CUDA(cudaMemcpyAsync(t, hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
+      EB_CUDA(cudaMemsetAsync((unsigned char*)t + CT_MPTR_OFF, 0, 8, st));
       void (*bk)(const uint32_t*, uint2*) = !P ? count_table_kernel<false, false>
                                                : (I ? count_table_kernel<true, true> : count_table_kernel<true, false>);
       const int nthr = 64 * 64 * 64 + 64 * 64 + 64;
@@ -2338,8 +2344,8 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
         h->launches += 1;
         EB_CUDA(cudaStreamSynchronize(st));
         h->ctab_m[v] = t;
+        EB_CUDA(cudaMemcpy((unsigned char*)h->ctab[v] + CT_MPTR_OFF, &h->ctab_m[v], 8, cudaMemcpyHostToDevice));
       }
-      A.ctab_m = (const uint2*)h->ctab_m[v];
     }
   }
   EB_CUDA(cudaMemsetAsync(d_counter, 0, 2 * sizeof(int), st));
