@@ -1,46 +1,60 @@
 #!/usr/bin/env python3
 """Benchmark: DFTSP instances/s on the config-2 Monte Carlo sweep (BASELINE.json).
 
-Workload (configs[1]): 10^6 synthetic scheduling instances, K = 20 admitted
-candidates each, BLOOM-3B with a uniform fp16 / w8a16 / w4a16-gptq mix on the
-paper's default edge node.  One step = one
-eb_dftsp_batch over this rank's shard of the instances.
+Workload (configs[1]): 10^6 synthetic scheduling instances per GPU, K = 20
+admitted candidates each, BLOOM-3B with a uniform fp16 / w8a16 / w4a16-gptq
+mix on the paper's default edge node.  One step
+= one eb_dftsp_batch over this rank's instances.
 
-  value   instances/s, inputs resident in HBM (EB_MEM_DEVICE), CUDA events on
-          the launch stream, L2 flushed between steps, max over ranks
-  e2e     same metric through the C ABI with HOST buffers (pinned): every step
-          copies the instances in and the results out inside the timed region
-  roofline  FP64 issue bound (the search is FP64 compare/accumulate + integer
-          control; no HBM or tensor-core bound applies), algorithmic FP64 ops
-          from the oracle's work counters on a sample of the same workload
-  cpu_baseline  the C oracle port of the reference on a bounded sample with all
-          host threads (rank 0, N=1)
+  value     instances/s, inputs resident in HBM (EB_MEM_DEVICE), CUDA events on
+            the launch stream, L2 flushed between steps, max over ranks
+  e2e       the same metric through the C ABI with HOST buffers (pinned), the
+            general request layout (eb_requests, what a caller hands over) and
+            the whole SearchOutcome read back (dftsp.py:42-51: status, z,
+            nodes visited/pruned, class counts, solution ids); every step's
+            copies are inside the timed region.  `e2e.wire` is the compact
+            wire format (eb_dftsp_batch_packed) with its host packing cost
+  roofline  FP64/issue bound of the search kernel: algorithmic FP64 ops per
+            instance (oracle work counters) over the kernel time, against the
+            FP64 add rate and the warp-instruction issue rate MEASURED in this
+            run by eb_probe_peaks; ncu-only counters come from the committed
+            capture and are flagged stale when the CUDA sources changed
+  cpu_baseline  the unmodified Python reference (oracle/_ref, its own
+            dftsp() with ProcessPoolExecutor(nproc), cli.py:262-264) on a
+            bounded sample of the same instances (rank 0, N=1); the C port of
+            it is reported beside (cpu_port) and checks the device on ALL
+            instances, every output field
 
-``--impl reference`` times the reference CPU path (oracle port, all host
-threads) on the same workload/metric and prints the same JSON line.
-Multi-GPU: torchrun, one rank per GPU, instances sharded by contiguous range
-(weak scaling: 10^6 instances per GPU), no data-path collective.
+``--impl reference`` times that Python reference on the same workload/metric
+and prints the same JSON line (rank 0 only; other ranks exit 0).  It rebuilds
+the identical 10^6 instances with the CPU admission oracle, so the CUDA
+library is never loaded on that arm.
+``--gpus N`` without torchrun re-launches itself under torch.distributed.run
+with N ranks (one per GPU, NCCL); instances are sharded by rank (weak scaling,
+10^6 per GPU), no data-path collective.
+``--config 5`` runs the tight-memory edge workload (configs[4]) instead;
+``--config 4`` the brute-force K=32 search sharded by subset rank over the
+ranks (configs[3], brute.solve_distributed).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "oracle"))   # CPU baseline / reference arm only
+sys.path.insert(0, os.path.join(ROOT, "oracle"))   # CPU baselines / checker only
 
-FP64_LANES_PER_SM = 64          # B200 FP64 pipe: 64 lanes/SM/clk
 LEAF_OPS, DESCEND_OPS = 26, 5   # algorithmic FP64-class ops per leaf check / descend
-LADDER = (128, 256, 512)
+METRIC = "DFTSP instances/sec (K=20 users) and search nodes/sec"
 
 
 def parse():
@@ -49,10 +63,73 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--config", type=int, default=2, choices=(2, 4, 5))
     ap.add_argument("--n-inst", type=int, default=1_000_000, help="instances per GPU")
-    ap.add_argument("--cpu-sample", type=int, default=0, help="instances in the CPU sample (0 = auto)")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="instances per reference step (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baselines (profiling runs)")
+    ap.add_argument("--brute-k", type=int, default=32)
+    ap.add_argument("--brute-n", type=int, default=8, help="config 4: instances per step")
     return ap.parse_args()
+
+
+# ---------------------------------------------------------------- plumbing --
+def self_spawn(args) -> int:
+    """--gpus N > 1 outside torchrun: re-launch under torch.distributed.run."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "WARN")
+    return subprocess.call(cmd, env=env)
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        if args.impl == "ours":
+            import torch
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend="nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend="gloo")
+    if world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} rank(s)", file=sys.stderr)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def ranks_info(world, dev):
+    """(distinct GPUs across ranks, NCCL communicator size) -- the scaling run's evidence."""
+    import torch
+    uuid = str(torch.cuda.get_device_properties(dev).uuid)
+    if world == 1:
+        return 1, 1
+    import torch.distributed as dist
+    got = [None] * world
+    dist.all_gather_object(got, uuid)
+    return len(set(got)), dist.get_world_size()
 
 
 def _nvml_sampler(idx: int, conn, stop, period: float):
@@ -87,7 +164,7 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []          # (time, sm_mhz, max_mhz, reasons bitmask)
+        self.rows = []
         self.t0 = self.t1 = None
         self.proc = None
 
@@ -140,149 +217,163 @@ class ClockSampler:
                 "window": "timed region" if in_window else "warm-up and timed region"}
 
 
-def dist_init(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch.distributed as dist
-        backend = "nccl" if args.impl == "ours" else "gloo"
-        dist.init_process_group(backend=backend)
-    return world, rank, local
-
-
-def barrier(world):
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-
-
-def max_over_ranks(x: float, world: int, device=None) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
-
-
-def profile_issue_pct():
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_dftsp_summary.json")) as fh:
-            return json.load(fh).get("issue_active_pct")
-    except (OSError, ValueError):
-        return None
-
-
-def profile_warp_inst():
-    """Warp instructions per instance of the search kernel (committed ncu capture)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_dftsp_summary.json")) as fh:
-            return json.load(fh).get("warp_instructions_per_instance")
-    except (OSError, ValueError):
-        return None
-
-
-def load_profile_traffic():
-    """DRAM bytes per launch of the search kernel from the committed ncu capture (or None)."""
-    p = os.path.join(ROOT, "profiles", "ncu_dftsp_summary.json")
-    try:
-        with open(p) as fh:
-            j = json.load(fh)
-        return j.get("dram_bytes_per_launch"), j.get("instances_per_launch")
-    except (OSError, ValueError):
-        return None, None
-
-
-def issue_roofline(sms: int, f_mhz: float, n: int, per_launch_s: float):
-    """Warp-instruction issue rate of the search kernel against the SM issue
-    peak (4 schedulers x 1 warp-instruction per clock per SM): the bound the
-    kernel actually meets.  Instructions per instance come from the committed
-    ncu capture; the time is this run's."""
-    wi = profile_warp_inst()
-    if not wi:
-        return None
-    achieved = wi * n / per_launch_s / 1e9
-    peak = sms * 4 * f_mhz * 1e6 / 1e9
-    out = {"achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "G warp-inst/s",
-           "frac": round(achieved / peak, 4), "warp_inst_per_instance_ncu": wi}
+def ncu_profile():
+    """The committed ncu capture of the search kernel, and whether it was taken on these sources."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_dftsp_summary.json")) as fh:
             j = json.load(fh)
-        # warp-execution efficiency (active lanes per issued warp instruction / 32)
-        # and the scenario-array stream rate, from the same capture
-        out["warp_execution_efficiency_ncu"] = round(j["threads_per_warp_inst"] / 32.0, 4)
-        out["hbm_gb_s_ncu"] = round(j["dram_bytes_per_launch"] / (j["duration_ms"] * 1e-3) / 1e9, 1)
-    except (OSError, ValueError, KeyError, TypeError, ZeroDivisionError):
-        pass
-    return out
+    except (OSError, ValueError):
+        return None, False
+    from paper_2405_07140_b200._build import source_hash
+    return j, j.get("source_hash") == source_hash()
 
 
-def cpu_baseline(batch, sample: int, threads: int):
+def workload(config: int):
+    from paper_2405_07140_b200 import synth
+    if config == 5:
+        return synth.CONFIG5, (64, 128, 256, 512, 1024)
+    return synth.CONFIG2, (128, 256, 512)
+
+
+def config_dict(w, ladder, n, world):
+    return {"workload": w.name, "instances_per_gpu": n, "K": w.K, "ladder": list(ladder),
+            "flags": "pruning=True inclusive=False exact_tau=False",
+            "l2": "flushed between steps (256 MiB write)", "parallelism": f"instance-sharded x{world}"}
+
+
+# ------------------------------------------------------------ reference arm --
+def reference_rate(batch, ladder, per_step: int, steps: int, warmup: int, procs: int):
+    """The Python reference's dftsp over consecutive slices of `batch`
+    (ProcessPoolExecutor(procs)); returns rate, spans, and agreement with the C
+    port on the instances it solved."""
     import oracle
+    import pyref
+    pool = pyref.ReferencePool(procs)
+    n = batch.n_inst
+    spans, vis_sum, done, agree = [], 0, 0, True
+    try:
+        for k in range(warmup + steps):
+            lo = (k * per_step) % max(1, n - per_step + 1)
+            span, z, vis, prn = pool.run(batch, lo, lo + per_step, ladder=ladder)
+            if k >= warmup:
+                spans.append(span)
+                vis_sum += int(vis.sum())
+                done += per_step
+                if len(spans) <= 2:     # the C port reproduces the reference on what it solved
+                    sub = slice_batch(batch, lo, lo + per_step)
+                    o = oracle.dftsp_batch(sub, ladder=ladder, threads=procs)
+                    agree &= bool(np.array_equal(o["z_found"], z) and np.array_equal(o["nodes_visited"], vis)
+                                  and np.array_equal(o["nodes_pruned"], prn))
+    finally:
+        pool.close()
+    t = sum(spans)
+    return done / t, vis_sum / t, t, agree
+
+
+def slice_batch(batch, lo, hi):
     from paper_2405_07140_b200.soa import InstanceBatch
-    n = min(sample, batch.n_inst)
-    sub = InstanceBatch(batch.offsets[:n + 1].copy(), {k: v[:int(batch.offsets[n])] for k, v in batch.columns.items()},
-                        batch.contexts, batch.ctx_index[:n].copy(), batch.k_max)
-    t0 = time.perf_counter()
-    res = oracle.dftsp_batch(sub, ladder=LADDER, threads=threads)
-    dt = time.perf_counter() - t0
-    return n / dt, dt, res, sub
+    r0, r1 = int(batch.offsets[lo]), int(batch.offsets[hi])
+    return InstanceBatch(batch.offsets[lo:hi + 1] - r0, {k: v[r0:r1] for k, v in batch.columns.items()},
+                         batch.contexts, batch.ctx_index[lo:hi].copy(), batch.k_max)
 
 
+def run_reference(args, world, rank):
+    """Reference CPU path: the unmodified Python reference (oracle/_ref) with
+    all host cores, on the same 10^6 instances (rebuilt with the CPU admission
+    oracle, so libedgebatch_b200.so is never loaded here)."""
+    if rank != 0:
+        return 0
+    import oracle
+    import pyref
+    from paper_2405_07140_b200 import synth
+    w, ladder = workload(args.config)
+    procs = os.cpu_count() or 1
+    base = {"metric": METRIC, "unit": "instances/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference"}
+    if args.config == 4:
+        base["unavailable"] = ("brute force K=28-32 is not timeable on the CPU reference (~20 h per instance "
+                               "per core, BASELINE.md §2c); the config-4 arm reports its extrapolation")
+        print(json.dumps(base), flush=True)
+        return 0
+    if not pyref.available():
+        base["unavailable"] = "oracle/_ref (the staged Python reference) is missing"
+        print(json.dumps(base), flush=True)
+        return 0
+    t0 = time.time()
+    batch = synth.generate(w, args.n_inst, seed=2405_07140, admit=oracle.admit)
+    gen_s = time.time() - t0
+    per_step = args.cpu_sample or procs * 60
+    rate, vis_rate, t, agree = reference_rate(batch, ladder, per_step, args.steps, args.warmup, procs)
+    line = dict(base)
+    line.update({
+        "value": round(rate, 2), "ms_per_step": round(t / args.steps * 1e3, 3),
+        "config": config_dict(w, ladder, args.n_inst, world),
+        "nodes_visited_per_s": round(vis_rate, 1),
+        "cpu_baseline": {"value": round(rate, 2), "unit": "instances/s", "cores": procs, "kind": "reference",
+                         "sample": f"{per_step} consecutive instances of the same {args.n_inst}-instance set per step, "
+                                   f"unmodified Python reference edgebatch.dftsp (oracle/_ref) in "
+                                   f"ProcessPoolExecutor({procs}); object construction untimed"},
+        "e2e": {"value": round(rate, 2), "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "c_port_agrees_with_reference": agree,
+        "same_instances": "synth.generate(seed=2405_07140) with the CPU admission oracle (device-identical)",
+        "gen_s": round(gen_s, 1),
+    })
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm --
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_spawn(args)
     world, rank, local = dist_init(args)
-    from paper_2405_07140_b200 import synth
-
     if args.impl == "reference":
         return run_reference(args, world, rank)
+    if args.config == 4:
+        return run_config4(args, world, rank, local)
+    return run_dftsp(args, world, rank, local)
+
+
+def run_dftsp(args, world, rank, local):
+    import ctypes
 
     import torch
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    from paper_2405_07140_b200 import _lib, search
-    from paper_2405_07140_b200.soa import search_params
+    from paper_2405_07140_b200 import _lib, synth
+    from paper_2405_07140_b200.soa import InstanceBatch, pack_wire, search_params
 
-    # ---- workload: this rank's shard (weak scaling: n_inst per GPU) --------
+    w, ladder = workload(args.config)
     t_gen = time.time()
-    batch = synth.generate(synth.CONFIG2, args.n_inst, seed=2405_07140 + rank, device=local)
+    batch = synth.generate(w, args.n_inst, seed=2405_07140 + rank, device=local)
     gen_s = time.time() - t_gen
     n, nr = batch.n_inst, batch.n_req
     h = _lib.handle(local)
     stream = torch.cuda.Stream(device=dev)
     h.set_stream(stream.cuda_stream)
 
-    # device-resident copies (value) and pinned host copies (e2e)
     def to_dev(a):
         return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
-    d_off = to_dev(batch.offsets)
-    d_ci = to_dev(batch.ctx_index)
     # dftsp reads every request column except `tolerance` (candidates are
     # already accuracy-admitted, sim.py:264-274), so it is not shipped
     used = [k for k in batch.columns if k != "tolerance"]
+    d_off, d_ci = to_dev(batch.offsets), to_dev(batch.ctx_index)
     d_cols = {k: to_dev(batch.columns[k]) for k in used}
     d_ctx = to_dev(batch.contexts.view(np.uint8)).contiguous()
-    outs = {"status": torch.zeros(n, dtype=torch.int32, device=dev),
-            "error_index": torch.zeros(n, dtype=torch.int32, device=dev),
-            "z_found": torch.zeros(n, dtype=torch.int32, device=dev),
-            "nodes_visited": torch.zeros(n, dtype=torch.int64, device=dev),
-            "nodes_pruned": torch.zeros(n, dtype=torch.int64, device=dev),
-            "n_classes": torch.zeros(n, dtype=torch.int32, device=dev),
-            "counts": torch.zeros(n * 16, dtype=torch.int32, device=dev),
-            "class_lengths": torch.zeros(n * 16, dtype=torch.int32, device=dev),
-            "solution": torch.zeros(nr, dtype=torch.int32, device=dev),
-            "metrics": torch.zeros(n * 8, dtype=torch.float64, device=dev)}
-    import ctypes
+    shapes = {"status": (n, torch.int32), "error_index": (n, torch.int32), "z_found": (n, torch.int32),
+              "nodes_visited": (n, torch.int64), "nodes_pruned": (n, torch.int64), "n_classes": (n, torch.int32),
+              "counts": (n * 16, torch.int32), "class_lengths": (n * 16, torch.int32),
+              "solution": (nr, torch.int32), "metrics": (n * 8, torch.float64)}
+    outs = {k: torch.zeros(m, dtype=t, device=dev) for k, (m, t) in shapes.items()}
     dres = _lib.eb_dftsp_result()
     for k, t in outs.items():
         setattr(dres, k, t.data_ptr())
-    from paper_2405_07140_b200.soa import InstanceBatch
     dbatch = InstanceBatch(d_off, d_cols, batch.contexts, d_ci, batch.k_max, on_device=True)
     db = dbatch.struct()
-    prm = search_params(ladder=LADDER)
+    prm = search_params(ladder=ladder)
     ref = lambda s: ctypes.cast(ctypes.pointer(s), ctypes.c_void_p)  # noqa: E731
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -290,18 +381,22 @@ def main():
         _lib.check(h.lib.eb_dftsp_batch(h.ptr, d_ctx.data_ptr(), len(batch.contexts), ref(prm), ref(db), ref(dres),
                                         _lib.EB_MEM_DEVICE), "eb_dftsp_batch")
 
+    # live roofline denominators (before the sampler: the probe is short)
+    fp64_peak = ctypes.c_double(0.0)
+    issue_peak = ctypes.c_double(0.0)
+    with torch.cuda.stream(stream):
+        _lib.check(h.lib.eb_probe_peaks(h.ptr, ctypes.byref(fp64_peak), ctypes.byref(issue_peak)), "eb_probe_peaks")
+
     clk = ClockSampler(local).start()
     with torch.cuda.stream(stream):
         # W warm-up steps, continued until the GPU has been busy for >= 1 s
-        # (the host-side workload generation leaves it idle long enough for
-        # the SM clock to drop; short runs would otherwise time the ramp)
+        # (host-side generation leaves it idle long enough for the SM clock to drop)
         t_w = time.perf_counter()
         done = 0
         while done < args.warmup or time.perf_counter() - t_w < 1.0:
             step_device()
             stream.synchronize()
             done += 1
-        stream.synchronize()
         barrier(world)
         torch.cuda.synchronize()
         launches0 = h.launches()
@@ -322,54 +417,50 @@ def main():
         launches = h.launches() - launches0
     dev_s = max_over_ranks(sum(times), world, dev)
     value = world * n * args.steps / dev_s
-    ms_per_step = dev_s / args.steps * 1e3
-    # device results for accounting (and a parity spot check against the oracle)
-    z = outs["z_found"].cpu().numpy()
-    vis = outs["nodes_visited"].cpu().numpy()
-    sol = outs["solution"].cpu().numpy()
-    owner = np.repeat(np.arange(n), np.diff(batch.offsets))
-    bits = np.where(sol >= 0, np.left_shift(np.int64(1), np.maximum(sol, 0).astype(np.int64)), 0)
-    sol_mask = np.zeros(n, np.int64)
-    np.bitwise_or.at(sol_mask, owner, bits)
-    status = outs["status"].cpu().numpy()
-    assert (status == 0).all(), f"device statuses: {np.unique(status)}"
+    res = {k: t.cpu().numpy() for k, t in outs.items()}
+    assert (res["status"] == 0).all(), f"device statuses: {np.unique(res['status'])}"
 
     # ---- e2e through the C ABI with pinned host buffers --------------------
     e2e = None
     if not args.no_e2e:
-        from paper_2405_07140_b200.soa import pack_wire
-
         def pinned(a):
             return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
 
-        # results a sweep consumes: status, z, node counts and the selected set
-        # (u64 mask per instance; the ids rise along the rows, so bit order is
-        # the solution's id order)
-        hout = {"status": torch.zeros(n, dtype=torch.int32).pin_memory(),
-                "z_found": torch.zeros(n, dtype=torch.int32).pin_memory(),
-                "nodes_visited": torch.zeros(n, dtype=torch.int64).pin_memory(),
-                "nodes_pruned": torch.zeros(n, dtype=torch.int64).pin_memory(),
-                "solution_mask": torch.zeros(n, dtype=torch.int64).pin_memory()}
+        # what SearchOutcome carries (dftsp.py:42-51): status, z, node counts,
+        # the class counts and the solution ids
+        hout = {"status": (n, torch.int32), "z_found": (n, torch.int32), "nodes_visited": (n, torch.int64),
+                "nodes_pruned": (n, torch.int64), "n_classes": (n, torch.int32), "counts": (n * 16, torch.int32),
+                "solution": (nr, torch.int32)}
+        hout = {k: torch.zeros(m, dtype=t).pin_memory() for k, (m, t) in hout.items()}
         hres = _lib.eb_dftsp_result()
         for k, t in hout.items():
             setattr(hres, k, t.data_ptr())
         d2h = sum(t.numel() * t.element_size() for t in hout.values())
-        # wide layout (eb_requests, 48 B/request) and the compact wire format
-        # (eb_requests_packed, 32 B/request); the same pinned output buffers
         hb = InstanceBatch(pinned(batch.offsets), {k: pinned(batch.columns[k]) for k in used}, batch.contexts,
                            pinned(batch.ctx_index), batch.k_max)
-        h2d_wide = sum(hb.columns[k].nbytes for k in used) + hb.offsets.nbytes + hb.ctx_index.nbytes
+        h2d = sum(hb.columns[k].nbytes for k in used) + hb.offsets.nbytes + hb.ctx_index.nbytes
+        hbs = hb.struct()
+        # wire variant: smaller output (mask) and a host packing cost, timed once
+        mout = {"status": torch.zeros(n, dtype=torch.int32).pin_memory(),
+                "z_found": torch.zeros(n, dtype=torch.int32).pin_memory(),
+                "nodes_visited": torch.zeros(n, dtype=torch.int64).pin_memory(),
+                "nodes_pruned": torch.zeros(n, dtype=torch.int64).pin_memory(),
+                "solution_mask": torch.zeros(n, dtype=torch.int64).pin_memory()}
+        mres = _lib.eb_dftsp_result()
+        for k, t in mout.items():
+            setattr(mres, k, t.data_ptr())
+        t_pack = time.perf_counter()
         wb = pack_wire(batch, pin=pinned)
-        assert wb is not None, "config-2 columns narrow losslessly"
-        hbs, wbs = hb.struct(), wb.struct()
+        pack_s = time.perf_counter() - t_pack
+        wbs = wb.struct() if wb is not None else None
 
-        def step_wide():
+        def step_general():
             _lib.check(h.lib.eb_dftsp_batch(h.ptr, batch.contexts.ctypes.data, len(batch.contexts), ref(prm),
                                             ref(hbs), ref(hres), _lib.EB_MEM_HOST), "eb_dftsp_batch(host)")
 
         def step_wire():
             _lib.check(h.lib.eb_dftsp_batch_packed(h.ptr, batch.contexts.ctypes.data, len(batch.contexts), ref(prm),
-                                                   ref(wbs), ref(hres), _lib.EB_MEM_HOST), "eb_dftsp_batch_packed")
+                                                   ref(wbs), ref(mres), _lib.EB_MEM_HOST), "eb_dftsp_batch_packed")
 
         def time_host(step):
             for _ in range(max(1, args.warmup)):
@@ -387,118 +478,172 @@ def main():
                 e1.record(stream)
                 e1.synchronize()
                 et.append(e0.elapsed_time(e1) / 1e3)
-            assert np.array_equal(hout["z_found"].numpy(), z) and np.array_equal(hout["nodes_visited"].numpy(), vis)
-            assert np.array_equal(hout["solution_mask"].numpy(), sol_mask)
             return max_over_ranks(sum(et), world, dev)
 
-        wide_s = time_host(step_wide)
-        wire_s = time_host(step_wire)
-        e2e = {"value": world * n * args.steps / wire_s, "unit": "instances/s", "h2d_bytes_per_step": int(wb.nbytes()),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": wire_s / args.steps * 1e3,
-               "path": "eb_dftsp_batch_packed(EB_MEM_HOST): pinned host buffers in the compact wire format "
-                       "(token counts as one dictionary byte, uniform uplink power, ids = row positions since "
-                       "they rise along every instance, uniform offsets): 25 B/request; uploads on their own "
-                       "stream, chunks ramping n/64 -> n/16 -> n/64 over 3 compute streams",
-               "wide": {"value": world * n * args.steps / wide_s, "h2d_bytes_per_step": int(h2d_wide),
-                        "ms_per_step": wide_s / args.steps * 1e3, "path": "eb_dftsp_batch(EB_MEM_HOST), eb_requests"}}
+        gen_s_e2e = time_host(step_general)
+        for k in hout:
+            assert np.array_equal(hout[k].numpy(), res[k]), f"e2e readback differs from the device run: {k}"
+        e2e = {"value": world * n * args.steps / gen_s_e2e, "unit": "instances/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": gen_s_e2e / args.steps * 1e3,
+               "path": "eb_dftsp_batch(EB_MEM_HOST): pinned host buffers in the general request layout "
+                       "(eb_requests columns the caller fills, 48 B/request) in; status, z, nodes visited/pruned, "
+                       "n_classes, counts[16] and the solution ids out; uploads on their own stream, chunks "
+                       "pipelined over 3 compute streams"}
+        if wbs is not None:
+            wire_s = time_host(step_wire)
+            owner = np.repeat(np.arange(n), np.diff(batch.offsets))
+            sol = res["solution"]
+            bits = np.where(sol >= 0, np.left_shift(np.int64(1), np.maximum(sol, 0).astype(np.int64)), 0)
+            sol_mask = np.zeros(n, np.int64)
+            np.bitwise_or.at(sol_mask, owner, bits)
+            assert np.array_equal(mout["solution_mask"].numpy(), sol_mask)
+            e2e["wire"] = {"value": world * n * args.steps / wire_s, "h2d_bytes_per_step": int(wb.nbytes()),
+                           "d2h_bytes_per_step": int(sum(t.numel() * t.element_size() for t in mout.values())),
+                           "ms_per_step": wire_s / args.steps * 1e3, "host_pack_s": round(pack_s, 3),
+                           "path": "eb_dftsp_batch_packed(EB_MEM_HOST): the compact wire format (token counts as "
+                                   "one dictionary byte, uniform uplink power, ids = row positions), valid only "
+                                   "for columns that narrow losslessly; solution as a u64 mask. host_pack_s "
+                                   "(soa.pack_wire, numpy) is NOT in the timed region"}
 
-    # ---- roofline (rank 0 figures) + cpu baseline ---------------------------
-    # (no collectives below: the other ranks are done; rank 0 has the host)
     clocks = clk.summary()
+    gpus_active, comm = ranks_info(world, dev)
     if rank != 0:
-        return
+        return 0
+
+    # ---- parity of every output field on ALL instances (C port, all threads)
     import oracle
-    sample = args.cpu_sample or (n if world == 1 else 50_000)     # N=1: the whole 10^6-instance workload
     threads = os.cpu_count() or 1
-    cpu_rate, cpu_s, orc, sub = cpu_baseline(batch, min(sample, n), threads)
-    parity_ok = bool(np.array_equal(orc["z_found"], z[:sub.n_inst]) and
-                     np.array_equal(orc["nodes_visited"], vis[:sub.n_inst]))
-    wsub = oracle.work_counters(InstanceBatch(sub.offsets[:20001], {k: v[:int(sub.offsets[min(20000, sub.n_inst)])]
-                                                                    for k, v in sub.columns.items()},
-                                              sub.contexts, sub.ctx_index[:20000], sub.k_max), ladder=LADDER,
-                                threads=threads)
-    n_w = min(20000, sub.n_inst)
-    ops_per_inst = (LEAF_OPS * wsub["leaf_checks"] + DESCEND_OPS * wsub["descends"]) / n_w
+    parity_ok, cpu_port = None, None
+    if not args.no_cpu:
+        t0 = time.perf_counter()
+        orc = oracle.dftsp_batch(batch, ladder=ladder, threads=threads)
+        port_s = time.perf_counter() - t0
+        cpu_port = {"value": round(n / port_s, 1), "unit": "instances/s", "cores": threads, "kind": "port",
+                    "sample": f"all {n} instances, C restatement of the reference (oracle/), {threads} threads"}
+        fields = ("status", "z_found", "nodes_visited", "nodes_pruned", "n_classes", "counts", "class_lengths",
+                  "solution", "metrics")
+        bad = [k for k in fields if not np.array_equal(np.asarray(orc[k]).reshape(-1), res[k].reshape(-1))]
+        parity_ok = not bad
+
+    # ---- roofline ----------------------------------------------------------
     props = torch.cuda.get_device_properties(dev)
     f_mhz = clocks.get("sm_max_mhz") or 1965.0
-    peak_fp64 = props.multi_processor_count * FP64_LANES_PER_SM * f_mhz * 1e6 / 1e12   # TFLOP/s (1 op/lane/clk)
+    nw = min(20000, n)
+    wsub = oracle.work_counters(slice_batch(batch, 0, nw), ladder=ladder, threads=threads)
+    ops_per_inst = (LEAF_OPS * wsub["leaf_checks"] + DESCEND_OPS * wsub["descends"]) / nw
     per_launch_s = dev_s / args.steps
     achieved = ops_per_inst * n / per_launch_s / 1e12
-    traffic, traffic_n = load_profile_traffic()
-    if traffic is not None and traffic_n:
-        traffic = traffic * n / traffic_n
+    peak = fp64_peak.value / 1e12
+    prof, current = ncu_profile()
+    issue = {"peak_measured": round(issue_peak.value / 1e9, 1),
+             "peak_nominal": round(props.multi_processor_count * 4 * f_mhz * 1e6 / 1e9, 1), "unit": "G warp-inst/s"}
+    traffic = None
+    if prof:
+        wi = prof.get("warp_instructions_per_instance")
+        if wi:
+            issue["achieved"] = round(wi * n / per_launch_s / 1e9, 1)
+            issue["frac"] = round(issue["achieved"] / issue["peak_measured"], 4)
+        issue["warp_inst_per_instance_ncu"] = wi
+        issue["warp_execution_efficiency_ncu"] = round(prof.get("threads_per_warp_inst", 0) / 32.0, 4)
+        issue["issue_active_pct_ncu"] = prof.get("issue_active_pct")
+        issue["ncu_capture_current"] = current
+        if prof.get("dram_bytes_per_launch") and prof.get("instances_per_launch"):
+            traffic = prof["dram_bytes_per_launch"] * n / prof["instances_per_launch"]
+
+    # ---- the reference CPU path (north-star denominator) -------------------
+    cpu = None
+    if not args.no_cpu and world == 1:
+        import pyref
+        if pyref.available():
+            per = args.cpu_sample or threads * 40
+            rate, _, t, agree = reference_rate(batch, ladder, per, 3, 1, threads)
+            cpu = {"value": round(rate, 2), "unit": "instances/s", "cores": threads, "kind": "reference",
+                   "sample": f"3 x {per} instances of this workload, unmodified Python reference edgebatch.dftsp "
+                             f"(oracle/_ref) in ProcessPoolExecutor({threads}), {t:.1f} s",
+                   "c_port_agrees_with_reference": agree}
+        else:
+            cpu = cpu_port
     line = {
-        "metric": "DFTSP instances/sec (K=20 users) and search nodes/sec",
-        "value": round(value, 1), "unit": "instances/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "warmup_steps_run": done, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": round(value, 1) if parity_ok is not False else None, "unit": "instances/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "warmup_steps_run": done,
+        "ms_per_step": round(dev_s / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": synth.CONFIG2.name, "instances_per_gpu": n, "K": 20, "ladder": list(LADDER),
-                   "flags": "pruning=True inclusive=False exact_tau=False", "l2": "flushed between steps (256 MiB)",
-                   "parallelism": f"instance-sharded x{world}"},
-        "nodes_visited_per_s": round(float(vis.sum()) * world * args.steps / dev_s, 1),
-        "mean_z": float(z.mean()), "mean_nodes_visited": float(vis.mean()),
+        "config": config_dict(w, ladder, n, world),
+        "nodes_visited_per_s": round(float(res["nodes_visited"].sum()) * world * args.steps / dev_s, 1),
+        "mean_z": float(res["z_found"].mean()), "mean_nodes_visited": float(res["nodes_visited"].mean()),
         "e2e": e2e,
         "gpu_launches": int(launches),
-        "roofline": {"bound": "fp64-issue", "achieved": round(achieved, 4), "peak": round(peak_fp64, 3),
-                     "unit": "TFLOP/s", "frac": round(achieved / peak_fp64, 5), "traffic": traffic,
+        "roofline": {"bound": "fp64-issue", "achieved": round(achieved, 4), "peak": round(peak, 3),
+                     "unit": "TFLOP/s", "frac": round(achieved / peak, 5), "traffic": traffic,
                      "ops_per_instance": round(ops_per_inst, 1),
-                     "ops_model": "26 FP64 ops per leaf check + 5 per descend (SURVEY.md 8(d)); counts from the "
-                                  "oracle on a 20k-instance sample of this workload; peak = SMs x 64 FP64 lanes x "
-                                  "max SM clock (no measured FP64 peak in MEASURED_PEAKS.json)",
-                     "issue_active_pct_ncu": profile_issue_pct(),
-                     "issue": issue_roofline(props.multi_processor_count, f_mhz, n, per_launch_s),
-                     "issue_note": "SM issue-slot utilisation of the search kernel from the committed ncu capture "
-                                   "(profiles/ncu_dftsp_summary.json): the path is instruction-issue bound "
-                                   "(integer control + FP64 compare/accumulate)"},
-        "cpu_baseline": {"value": round(cpu_rate, 1), "unit": "instances/s", "cores": threads, "kind": "port",
-                         "sample": f"{sub.n_inst} instances of the same workload, C oracle (literal restatement "
-                                   f"of the reference), {threads} threads, {cpu_s:.1f} s"},
-        "parity_sample_ok": parity_ok,
+                     "ops_model": "26 FP64 ops per leaf check + 5 per descend of the REFERENCE algorithm (SURVEY.md "
+                                  "8(d)), counted by the oracle on 20k instances of this workload; the device "
+                                  "skips provably failing calls, so this is a reference-equivalent rate; peak = "
+                                  "FP64 add rate measured in this run (eb_probe_peaks)",
+                     "issue": issue},
+        "cpu_baseline": cpu, "cpu_port": cpu_port,
+        "parity": {"ok": parity_ok, "instances": n if parity_ok is not None else 0,
+                   "fields": "status z nodes_visited nodes_pruned n_classes counts class_lengths solution metrics"},
+        "gpus_active": gpus_active, "comm_nranks": comm,
         "clocks": clocks,
         "gen_s": round(gen_s, 1),
     }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-
-
-def run_reference(args, world, rank):
-    """Reference CPU path (C oracle port of the reference, all host threads) on this workload."""
-    if rank != 0:
-        return
-    import oracle
-    from paper_2405_07140_b200 import synth
-    try:
-        import torch
-        if not torch.cuda.is_available():
-            raise RuntimeError
-        batch_src = "device-admitted synthetic workload"
-    except Exception:
-        batch_src = None
-    # up to the same 10^6 instances per step, bounded so that the whole
-    # warm-up + timed run stays near a minute (~2.6e5 inst/s on 16 threads)
-    sample = args.cpu_sample or min(1_000_000, max(50_000, int(15e6 / max(1, args.steps + args.warmup))))
-    batch = synth.generate(synth.CONFIG2, sample, seed=2405_07140)
-    threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        oracle.dftsp_batch(batch, ladder=LADDER, threads=threads)
-    t = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        res = oracle.dftsp_batch(batch, ladder=LADDER, threads=threads)
-        t.append(time.perf_counter() - t0)
-    rate = batch.n_inst * args.steps / sum(t)
-    line = {"metric": "DFTSP instances/sec (K=20 users) and search nodes/sec", "value": round(rate, 1),
-            "unit": "instances/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(sum(t) / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": synth.CONFIG2.name, "K": 20, "sample_instances": batch.n_inst,
-                       "source": batch_src},
-            "nodes_visited_per_s": round(float(res["nodes_visited"].sum()) * args.steps / sum(t), 1),
-            "cpu_baseline": {"value": round(rate, 1), "unit": "instances/s", "cores": threads, "kind": "port",
-                             "sample": f"{batch.n_inst} instances per step, C oracle port, {threads} threads"},
-            "e2e": {"value": round(rate, 1), "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if parity_ok is False:
+        line["parity"]["mismatched"] = bad
     print(json.dumps(line), flush=True)
+    return 0 if parity_ok is not False else 1
+
+
+def run_config4(args, world, rank, local):
+    """Brute force (exhaustive_optimal subsets mode, dftsp.py:288-313) at K =
+    --brute-k over the adversarial family, every level's rank range sharded
+    over the ranks; one 8-byte all-reduce(MIN) per live level."""
+    import torch
+    torch.cuda.set_device(local)
+    from paper_2405_07140_b200 import brute, synth
+    K = args.brute_k
+    insts = synth.brute_family(K, args.brute_n, seed=2405_07140)
+    clk = ClockSampler(local).start()
+    for rec, cols in insts[:min(len(insts), max(1, args.warmup))]:
+        brute.solve_distributed(rec, cols) if world > 1 else brute.solve_sharded(rec, cols, 1, device=local)
+    barrier(world)
+    torch.cuda.synchronize()
+    clk.begin()
+    stats0 = brute.enum_stats(local)
+    t0 = time.perf_counter()
+    out = []
+    for _ in range(args.steps):
+        for rec, cols in insts:
+            r = brute.solve_distributed(rec, cols) if world > 1 else brute.solve_sharded(rec, cols, 1, device=local)
+            out.append((r.z, r.lexrank, r.nodes_visited, r.mask))
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    clk.end()
+    stats = brute.enum_stats(local) - stats0
+    wall = max_over_ranks(wall, world, torch.device("cuda", local))
+    checked = torch.tensor([float(stats[0]), float(stats[1])], dtype=torch.float64, device=torch.device("cuda", local))
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(checked)
+    clocks = clk.summary()
+    gpus_active, comm = ranks_info(world, torch.device("cuda", local))
+    if rank != 0:
+        return 0
+    n_solved = args.steps * len(insts)
+    line = {"metric": "brute-force exhaustive_optimal instances/sec (K=%d) and checked subsets/sec" % K,
+            "value": round(n_solved / wall, 4), "unit": "instances/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config4: brute force 2^K, K={K}, adversarial family (synth.brute_family)",
+                       "instances_per_step": len(insts), "parallelism": f"subset-rank-sharded x{world}"},
+            "checked_subsets_per_s": round(float(checked[0].item()) / wall, 1),
+            "pruned_prefixes_per_s": round(float(checked[1].item()) / wall, 1),
+            "reference_nodes_per_s": round(sum(o[2] for o in out[:len(insts)]) * args.steps / wall, 1),
+            "results": [list(o) for o in out[:len(insts)]],
+            "gpus_active": gpus_active, "comm_nranks": comm, "clocks": clocks}
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -51,7 +51,8 @@ typedef enum eb_status {
   EB_ERR_CAP_EXCEEDED = 16,        /* ValueError            dftsp.py:302-303        */
   EB_ERR_OVERFLOW = 17,            /* exact integer FLOP count would exceed int64    */
   EB_ERR_BAD_MODE = 18,            /* ValueError            dftsp.py:314-315        */
-  EB_ERR_PADDED_TOO_SMALL = 19     /* ValueError            feasibility.py:142-143  */
+  EB_ERR_PADDED_TOO_SMALL = 19,    /* ValueError            feasibility.py:142-143  */
+  EB_ERR_NONPOSITIVE_LINK = 20     /* ValueError            radio.py:63-64 (power, gain or noise <= 0) */
 } eb_status;
 
 typedef enum eb_mem { EB_MEM_HOST = 0, EB_MEM_DEVICE = 1 } eb_mem;
@@ -176,6 +177,10 @@ int32_t eb_handle_set_stream(eb_handle *h, void *stream);
 int32_t eb_synchronize(eb_handle *h);
 /* Kernels launched by this handle since creation (evidence counter). */
 int64_t eb_kernel_launches(eb_handle *h);
+/* Live roofline denominators (bench.py): FP64 add rate (DADD/s over every SM)
+ * and warp-instruction issue rate (independent IMAD + LOP3 chains) measured on
+ * the handle's GPU at its current clocks.  No reference counterpart. */
+int32_t eb_probe_peaks(eb_handle *h, double *fp64_ops_per_s, double *warp_inst_per_s);
 
 /* ---- K3: instance-parallel DFTSP -------------------------------------
  * Replaces dftsp() dftsp.py:237-285 (with derive_coefficients

@@ -62,6 +62,8 @@ def load():
         lib.oracle_exhaustive_counts.argtypes = [P, P, I32, P, P, P, P, P, P, P, P, P, P]
         lib.oracle_nob.restype = None
         lib.oracle_nob.argtypes = [P, I32, P, P, P, F64, F64, I32, P, P, P, P]
+        lib.oracle_admission_batch.restype = I32
+        lib.oracle_admission_batch.argtypes = [P, I32, P, I32, I32, P, P, I32]
         _o = lib
     return _o
 
@@ -157,3 +159,21 @@ def exhaustive_counts(ctx_rec, cols, lo, hi, ladder=None):
                                       a["channel_gain"].ctypes.data, a["uplink_power_w"].ctypes.data,
                                       C.byref(z), C.byref(nodes), sol.ctypes.data)
     return st, z.value, nodes.value, tuple(int(x) for x in sol[:z.value])
+
+
+def admission_batch(batch: InstanceBatch, accuracy_check=True, prefilter=True, threads=None):
+    """Oracle sim._dftsp_candidates (sim.py:264-274) per row: (status, keep)."""
+    lib = load()
+    nr = batch.n_req
+    status = np.zeros(max(nr, 1), np.int32)
+    keep = np.zeros(max(nr, 1), np.uint8)
+    b = batch.struct()
+    lib.oracle_admission_batch(batch.contexts.ctypes.data, len(batch.contexts), _ref(b), int(accuracy_check),
+                               int(prefilter), status.ctypes.data, keep.ctypes.data,
+                               int(threads or os.cpu_count() or 1))
+    return status[:nr], keep[:nr]
+
+
+def admit(batch: InstanceBatch, recs):
+    """synth.generate's admission hook computed by the oracle (no device)."""
+    return admission_batch(batch)

@@ -77,6 +77,32 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def source_hash() -> str:
+    """sha256 (16 hex) over the CUDA sources and the ABI header: ties a
+    committed ncu capture to the kernels it measured (bench.py flags
+    captures of other sources as stale)."""
+    import hashlib
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                   glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(ROOT, "include", "edgebatch_b200.h")]
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def stage_reference() -> str | None:
+    """Test-only: stage the unmodified Python reference into oracle/_ref
+    (oracle/make_ref.py; a no-op where /root/reference is absent)."""
+    sys.path.insert(0, ORACLE_DIR)
+    try:
+        import make_ref
+        return make_ref.stage()
+    finally:
+        sys.path.remove(ORACLE_DIR)
+
+
 def build_oracle(force: bool = False) -> str:
     """Test-only: compile the CPU oracle (oracle/edgebatch_oracle.c)."""
     src = os.path.join(ORACLE_DIR, "edgebatch_oracle.c")

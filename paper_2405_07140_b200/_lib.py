@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import threading
 
 import numpy as np
@@ -39,6 +40,7 @@ ERR_CAP_EXCEEDED = 16
 ERR_OVERFLOW = 17
 ERR_BAD_MODE = 18
 ERR_PADDED_TOO_SMALL = 19
+ERR_NONPOSITIVE_LINK = 20
 
 MET_UP_SUM, MET_DN_SUM, MET_MEM_POOLPAD, MET_LAT_POOLPAD, MET_MEM_BATCHPAD, MET_LAT_BATCHPAD, \
     MET_PADDED, MET_WIN_D = range(8)
@@ -113,6 +115,7 @@ _SIGS = {
     "eb_handle_set_stream": (I32, [P, P]),
     "eb_synchronize": (I32, [P]),
     "eb_kernel_launches": (I64, [P]),
+    "eb_probe_peaks": (I32, [P, P, P]),
     "eb_dftsp_batch": (I32, [P, P, I32, P, P, P, I32]),
     "eb_dftsp_batch_packed": (I32, [P, P, I32, P, P, P, I32]),
     "eb_dfs_single": (I32, [P, I32, I32, P, P, P, P, P, P, P, P, I64, I32, F64, P, P, P, P, P]),
@@ -205,9 +208,23 @@ class Handle:
             pass
 
 
+def default_device() -> int:
+    """The calling process's GPU: torch's current device once torch has
+    initialised CUDA, else LOCAL_RANK (one process per GPU under torchrun),
+    else 0."""
+    torch = sys.modules.get("torch")
+    if torch is not None:
+        try:
+            if torch.cuda.is_initialized():
+                return int(torch.cuda.current_device())
+        except Exception:
+            pass
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
 def handle(device: int | None = None) -> Handle:
     """Per-thread default handle (the library keeps no global mutable state)."""
-    dev = 0 if device is None else device
+    dev = default_device() if device is None else device
     hs = getattr(_tls, "handles", None)
     if hs is None:
         hs = _tls.handles = {}

@@ -79,6 +79,8 @@ def device_level_range(ctx_rec: np.ndarray, cols: dict, device=None):
     ref = ctypes.cast(ctypes.pointer(rs), ctypes.c_void_p)
 
     def raise_link(code):
+        if code == _lib.ERR_NONPOSITIVE_LINK:
+            raise ValueError("power, gain and noise must be strictly positive")
         if code in (_lib.ERR_UPLINK_EFF_ZERO, _lib.ERR_DOWNLINK_EFF_ZERO):
             raise ValueError("uplink spectral efficiency is zero" if code == _lib.ERR_UPLINK_EFF_ZERO
                              else "downlink spectral efficiency is zero")
@@ -136,24 +138,35 @@ def solve_sharded(ctx_rec, cols: dict, world: int, level=None, device=None) -> B
 
 
 def solve_distributed(ctx_rec, cols: dict, level=None, device=None, group=None) -> BruteResult:
-    """One shard per torch.distributed rank; a single all-reduce(MAX) of the packed key."""
+    """One shard of every level per torch.distributed rank, levels z = K..1.
+
+    The levels the sound bounds refute are skipped by every rank alike (the
+    live mask is computed from the same data on each rank, no exchange).  On
+    each live level every rank scans its contiguous rank range, then one
+    8-byte all-reduce(MIN) of the first feasible rank found (or a sentinel)
+    decides the level for all ranks together: the first level with any hit is
+    z*, the minimum is r*, and no rank descends further alone.
+    """
     import torch
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     n = int(cols["prompt_tokens"].shape[0])
+    if device is None and dist.get_backend(group) == "nccl":
+        device = torch.cuda.current_device()
     level = level or device_level_range(ctx_rec, cols, device)
-    z, r = local_search(n, world, rank, level)
+    live = getattr(level, "live_mask", (1 << n) - 1)
     on_gpu = dist.get_backend(group) == "nccl"
     tdev = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
-    if n <= 56:
-        key = torch.tensor([pack(z, r)], dtype=torch.int64, device=tdev)
-        dist.all_reduce(key, op=dist.ReduceOp.MAX, group=group)
-        zg, rg = unpack(int(key.item()))
-    else:
-        t = torch.tensor([z], dtype=torch.int64, device=tdev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-        zg = int(t.item())
-        rr = torch.tensor([r if (z == zg and zg) else 2 ** 62], dtype=torch.int64, device=tdev)
-        dist.all_reduce(rr, op=dist.ReduceOp.MIN, group=group)
-        rg = int(rr.item()) if zg else -1
-    return finish(n, zg, rg)
+    none = 2 ** 63 - 1
+    key = torch.empty(1, dtype=torch.int64, device=tdev)
+    for z in range(n, 0, -1):
+        if not (live >> (z - 1)) & 1:
+            continue
+        lo, hi = shard(comb(n, z), world, rank)
+        r = level(z, lo, hi) if hi > lo else -1
+        key.fill_(r if r >= 0 else none)
+        dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
+        rg = int(key.item())
+        if rg != none:
+            return finish(n, z, rg)
+    return finish(n, 0, -1)

@@ -476,6 +476,7 @@ const char* eb_status_string(int32_t s) {
     case EB_ERR_OVERFLOW: return "integer cost model would overflow int64";
     case EB_ERR_BAD_MODE: return "unknown exhaustive mode";
     case EB_ERR_PADDED_TOO_SMALL: return "padded_len must cover every candidate prompt";
+    case EB_ERR_NONPOSITIVE_LINK: return "power, gain and noise must be strictly positive";
     default: return "unknown status";
   }
 }

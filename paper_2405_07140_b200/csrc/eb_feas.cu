@@ -24,13 +24,20 @@ __global__ void link_kernel(const eb_context* ctxs, int n_ctx, eb_requests req, 
     double* o = out + 6 * j;
     if (ci < 0) { status[j] = EB_ERR_INVALID_ARG; continue; }
     const Ctx c = load_ctx(&ctxs[ci]);
-    double g = req.channel_gain[j];
-    double eu = spectral_efficiency(req.uplink_power_w[j], g, c.N0_up);
-    double ed = spectral_efficiency(c.P_dn, g, c.N0_dn);
+    double g = req.channel_gain[j], pu = req.uplink_power_w[j];
     int st = 0;
-    double ku = 0.0, kd = 0.0;
-    if (eu <= 0.0) st = EB_ERR_UPLINK_EFF_ZERO; else ku = fraction_per_token(c.fbits, c.T_up, c.B_up, eu);
-    if (ed <= 0.0) { if (!st) st = EB_ERR_DOWNLINK_EFF_ZERO; } else kd = fraction_per_token(c.fbits, c.T_dn, c.B_dn, ed);
+    double eu = 0.0, ed = 0.0, ku = 0.0, kd = 0.0;
+    // radio.py:63-64: nonpositive power/gain/noise raise before log2
+    if (pu <= 0.0 || g <= 0.0 || c.N0_up <= 0.0) st = EB_ERR_NONPOSITIVE_LINK;
+    else {
+      eu = spectral_efficiency(pu, g, c.N0_up);
+      if (eu <= 0.0) st = EB_ERR_UPLINK_EFF_ZERO; else ku = fraction_per_token(c.fbits, c.T_up, c.B_up, eu);
+    }
+    if (c.P_dn <= 0.0 || g <= 0.0 || c.N0_dn <= 0.0) { if (!st) st = EB_ERR_NONPOSITIVE_LINK; }
+    else {
+      ed = spectral_efficiency(c.P_dn, g, c.N0_dn);
+      if (ed <= 0.0) { if (!st) st = EB_ERR_DOWNLINK_EFF_ZERO; } else kd = fraction_per_token(c.fbits, c.T_dn, c.B_dn, ed);
+    }
     o[0] = eu; o[1] = ed; o[2] = ku; o[3] = kd;
     o[4] = mul(i2d(req.prompt_tokens[j]), ku);   // min_uplink_fraction radio.py:87-94
     o[5] = mul(i2d(req.output_tokens[j]), kd);   // min_downlink_fraction radio.py:97-101

@@ -40,7 +40,10 @@ __device__ __forceinline__ Ctx load_ctx(const eb_context* __restrict__ p) {
 }
 
 // uplink_fraction_per_token radio.py:71-76; returns status (0 ok).
+// spectral_efficiency radio.py:63-64 raises ValueError("power, gain and noise
+// must be strictly positive") first; `<= 0` is false for NaN, as in Python.
 __device__ __forceinline__ int k_up_of(const Ctx& c, double gain, double pup, double* out) {
+  if (pup <= 0.0 || gain <= 0.0 || c.N0_up <= 0.0) { *out = 0.0; return EB_ERR_NONPOSITIVE_LINK; }
   double eff = spectral_efficiency(pup, gain, c.N0_up);
   if (eff <= 0.0) { *out = 0.0; return EB_ERR_UPLINK_EFF_ZERO; }    // radio.py:74
   *out = fraction_per_token(c.fbits, c.T_up, c.B_up, eff);
@@ -48,6 +51,7 @@ __device__ __forceinline__ int k_up_of(const Ctx& c, double gain, double pup, do
 }
 // downlink_fraction_per_token radio.py:79-84
 __device__ __forceinline__ int k_dn_of(const Ctx& c, double gain, double* out) {
+  if (c.P_dn <= 0.0 || gain <= 0.0 || c.N0_dn <= 0.0) { *out = 0.0; return EB_ERR_NONPOSITIVE_LINK; }
   double eff = spectral_efficiency(c.P_dn, gain, c.N0_dn);
   if (eff <= 0.0) { *out = 0.0; return EB_ERR_DOWNLINK_EFF_ZERO; }  // radio.py:82
   *out = fraction_per_token(c.fbits, c.T_dn, c.B_dn, eff);

@@ -1,0 +1,95 @@
+// eb_probe.cu -- live roofline denominators for bench.py (no profiler).
+//
+// The search kernels are bound by SM instruction issue on FP64
+// compare/accumulate plus integer control, and
+// MEASURED_PEAKS.json carries only HBM and bf16 figures.  These two probes
+// measure, on the calling GPU at its current clocks, (a) the FP64 add rate
+// (independent DADD chains on every SM) and (b) the warp-instruction issue
+// rate (independent integer chains, 4 schedulers per SM), so the bench line's
+// fractions are "of measured", not nominal.
+#include "eb_internal.cuh"
+
+namespace eb {
+namespace {
+
+constexpr int kChains = 8;
+
+__global__ void __launch_bounds__(256) probe_dadd_kernel(int iters, double seed, double* sink) {
+  double a[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) a[c] = seed + threadIdx.x * 1e-9 + c;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) a[c] = __dadd_rn(a[c], 1.0000000001);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += a[c];
+  if (s == -1.0) sink[0] = s;   // never true; keeps the chains live
+}
+
+// 4 IMAD chains (fma pipe) + 4 LOP3 chains (alu pipe) per step: 8 SASS
+// instructions, half on each pipe, so the pair can issue every cycle
+// (B300_MICROARCH.md "Pipe rates": each pipe alone sustains 1 per 2 cycles).
+// The volatile asm keeps the compiler from folding the loop.
+__global__ void __launch_bounds__(256) probe_issue_kernel(int iters, unsigned seed, unsigned* sink) {
+  unsigned m[4], x[4];
+  unsigned mul = seed | 1u, inc = seed * 7u + 3u;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) { m[c] = seed + threadIdx.x + c; x[c] = seed ^ (threadIdx.x * 31u + c); }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(m[c]) : "r"(mul), "r"(inc));
+      // (x & m) | inc: two consecutive steps involve 4 inputs, so no single LOP3 fuses them
+      asm volatile("{ .reg .u32 t; and.b32 t, %0, %1; or.b32 %0, t, %2; }" : "+r"(x[c]) : "r"(m[c]), "r"(inc));
+    }
+  }
+  unsigned s = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) s ^= m[c] ^ x[c];
+  if (s == 0x12345678u) sink[0] = s;
+}
+
+}  // namespace
+}  // namespace eb
+
+extern "C" int32_t eb_probe_peaks(eb_handle* h, double* fp64_ops_per_s, double* warp_inst_per_s) {
+  if (!h || !fp64_ops_per_s || !warp_inst_per_s) return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  void* sink = nullptr;
+  EB_CUDA(cudaMallocAsync(&sink, 64, st));
+  cudaEvent_t e0, e1;
+  EB_CUDA(cudaEventCreate(&e0));
+  EB_CUDA(cudaEventCreate(&e1));
+  const int blocks = h->num_sms * 8, threads = 256, iters = 1 << 14;
+  float best_d = 1e30f, best_i = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {   // the first rep ramps clocks
+    float ms = 0.f;
+    EB_CUDA(cudaEventRecord(e0, st));
+    eb::probe_dadd_kernel<<<blocks, threads, 0, st>>>(iters, 1.0 + rep, (double*)sink);
+    EB_CUDA(cudaEventRecord(e1, st));
+    EB_CUDA(cudaEventSynchronize(e1));
+    EB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep) best_d = ms < best_d ? ms : best_d;
+    EB_CUDA(cudaEventRecord(e0, st));
+    eb::probe_issue_kernel<<<blocks, threads, 0, st>>>(iters, 7u + rep, (unsigned*)sink);
+    EB_CUDA(cudaEventRecord(e1, st));
+    EB_CUDA(cudaEventSynchronize(e1));
+    EB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep) best_i = ms < best_i ? ms : best_i;
+    h->launches += 2;
+  }
+  EB_CUDA(cudaGetLastError());
+  EB_CUDA(cudaEventDestroy(e0));
+  EB_CUDA(cudaEventDestroy(e1));
+  EB_CUDA(cudaFreeAsync(sink, st));
+  EB_CUDA(cudaStreamSynchronize(st));
+  const double thr = (double)blocks * threads;
+  *fp64_ops_per_s = thr * iters * eb::kChains / (best_d * 1e-3);
+  // 8 warp instructions per loop step (4 IMAD + 4 LOP3; tests/test_abi.py
+  // checks the SASS mix)
+  *warp_inst_per_s = thr / 32.0 * iters * 8.0 / (best_i * 1e-3);
+  return EB_OK;
+}

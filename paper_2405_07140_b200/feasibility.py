@@ -118,6 +118,8 @@ def raise_for_status(status: int, reqs=None, err_index: int = -1, ctx=None, ladd
         m1 = weight_bytes(ctx.llm)
         raise WeightsDoNotFitError(f"weights need {m1} bytes but only "
                                    f"{ctx.node.memory_bytes / ctx.quant.alpha:.4g} scaled bytes are available")
+    if status == _lib.ERR_NONPOSITIVE_LINK:
+        raise ValueError("power, gain and noise must be strictly positive")
     if status == _lib.ERR_UPLINK_EFF_ZERO:
         raise ValueError("uplink spectral efficiency is zero")
     if status == _lib.ERR_DOWNLINK_EFF_ZERO:

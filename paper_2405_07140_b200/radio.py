@@ -104,6 +104,8 @@ def _as_ref(struct):
 
 
 def _raise_link(status: int) -> None:
+    if status == _lib.ERR_NONPOSITIVE_LINK:
+        raise ValueError("power, gain and noise must be strictly positive")
     if status == _lib.ERR_UPLINK_EFF_ZERO:
         raise ValueError("uplink spectral efficiency is zero")
     if status == _lib.ERR_DOWNLINK_EFF_ZERO:
@@ -133,7 +135,18 @@ def spectral_efficiency(power_w: float, channel_gain: float, noise_w: float) -> 
     return float(out[0, 0])
 
 
+def _check_up(link, cfg) -> None:
+    if link.uplink_power_w <= 0 or link.channel_gain <= 0 or cfg.uplink_noise_w <= 0:
+        _raise_link(_lib.ERR_NONPOSITIVE_LINK)        # radio.py:63-64
+
+
+def _check_dn(link, cfg) -> None:
+    if cfg.downlink_power_w <= 0 or link.channel_gain <= 0 or cfg.downlink_noise_w <= 0:
+        _raise_link(_lib.ERR_NONPOSITIVE_LINK)
+
+
 def uplink_fraction_per_token(link, cfg) -> float:
+    _check_up(link, cfg)
     st, out = _one(link, cfg)
     if st == _lib.ERR_UPLINK_EFF_ZERO:
         _raise_link(st)
@@ -141,6 +154,7 @@ def uplink_fraction_per_token(link, cfg) -> float:
 
 
 def downlink_fraction_per_token(link, cfg) -> float:
+    _check_dn(link, cfg)
     st, out = _one(link, cfg)
     if out[1] <= 0.0:
         _raise_link(_lib.ERR_DOWNLINK_EFF_ZERO)
@@ -150,6 +164,7 @@ def downlink_fraction_per_token(link, cfg) -> float:
 def min_uplink_fraction(prompt_tokens: int, link, cfg) -> float:
     if prompt_tokens < 0:
         raise ValueError("prompt_tokens must be nonnegative")
+    _check_up(link, cfg)
     st, out = _one(link, cfg, prompt=prompt_tokens)
     if st == _lib.ERR_UPLINK_EFF_ZERO:
         _raise_link(st)
@@ -159,6 +174,7 @@ def min_uplink_fraction(prompt_tokens: int, link, cfg) -> float:
 def min_downlink_fraction(output_tokens: int, link, cfg) -> float:
     if output_tokens < 0:
         raise ValueError("output_tokens must be nonnegative")
+    _check_dn(link, cfg)
     st, out = _one(link, cfg, output=output_tokens)
     if out[1] <= 0.0:
         _raise_link(_lib.ERR_DOWNLINK_EFF_ZERO)

@@ -71,7 +71,7 @@ def partition(pool, radio, ladder=None) -> ClassPartition:
                          [r.prompt_tokens for r in pool], [r.output_tokens for r in pool], _radio_ctx(radio))
     groups: dict = {}
     for j, r in enumerate(pool):
-        if st[j] == _lib.ERR_UPLINK_EFF_ZERO:
+        if st[j] in (_lib.ERR_UPLINK_EFF_ZERO, _lib.ERR_NONPOSITIVE_LINK):
             _raise_link(int(st[j]))
         groups.setdefault(r.output_tokens, []).append((float(out[j, 4]), r.id, j))
     lengths = tuple(sorted(groups))

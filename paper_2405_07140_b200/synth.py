@@ -5,7 +5,7 @@ already passed the simulator's admission (``sim._dftsp_candidates``,
 sim.py:264-274: accuracy filter + alone-feasible prefilter).  Requests are
 drawn with numpy (prompt, output, deadline*scale, tolerance*cap, Rayleigh
 gain, waiting ~ U[0, epoch)) in vectorised rounds; admission is decided
-exactly on the GPU by the K1 kernel (``eb_admission_batch``); the first K
+exactly on the GPU by the K1 kernel (``eb_admission_batch``) by default; the first K
 admitted draws of each instance are kept, ids 0..K-1 in acceptance order.
 """
 from __future__ import annotations
@@ -83,15 +83,40 @@ def _draw(rng, n, w: Workload):
     }
 
 
-def generate(w: Workload, n_inst: int, seed: int = 2405_07140, chunk: int = 100_000, device=None) -> InstanceBatch:
-    """n_inst instances of exactly w.K admitted candidates each (host arrays)."""
+def device_admission(device=None):
+    """K1 admission hook on the GPU: (batch, recs) -> (status, keep) per row."""
+    h = _lib.handle(device)
+
+    def admit(batch: InstanceBatch, recs):
+        nr = batch.n_req
+        status = np.zeros(nr, np.int32)
+        keep = np.zeros(nr, np.uint8)
+        b = batch.struct()
+        _lib.check(h.lib.eb_admission_batch(h.ptr, recs.ctypes.data, len(recs),
+                                            ctypes.cast(ctypes.pointer(b), ctypes.c_void_p), 1, 1,
+                                            status.ctypes.data, keep.ctypes.data, _lib.EB_MEM_HOST),
+                   "eb_admission_batch")
+        return status, keep
+
+    return admit
+
+
+def generate(w: Workload, n_inst: int, seed: int = 2405_07140, chunk: int = 100_000, device=None,
+             admit=None) -> InstanceBatch:
+    """n_inst instances of exactly w.K admitted candidates each (host arrays).
+
+    ``admit(batch, recs) -> (status, keep)`` decides admission per drawn row;
+    the default is the device K1 kernel.  Any admission with the reference's
+    decisions yields the identical batch (the draws depend only on the seed
+    and the keep decisions), which is how the CPU reference arm rebuilds the
+    same instances without the CUDA library (bench.py --impl reference)."""
     recs = contexts(w)
+    admit = admit or device_admission(device)
     rng = np.random.default_rng(seed)
     prof = rng.integers(0, len(w.profiles), size=n_inst).astype(np.int32)
     K = w.K
     out = {name: np.empty(n_inst * K, dt) for name, dt in REQ_FIELDS}
     p_up = dbm(20.0)
-    h = _lib.handle(device)
     for c0 in range(0, n_inst, chunk):
         c1 = min(n_inst, c0 + chunk)
         m = c1 - c0
@@ -112,13 +137,7 @@ def generate(w: Workload, n_inst: int, seed: int = 2405_07140, chunk: int = 100_
             ci = prof[c0 + act]
             batch = InstanceBatch(off, {k: np.ascontiguousarray(v) for k, v in cols.items()}, recs,
                                   np.ascontiguousarray(ci), int(R.max()))
-            status = np.zeros(nr, np.int32)
-            keep = np.zeros(nr, np.uint8)
-            b = batch.struct()
-            _lib.check(h.lib.eb_admission_batch(h.ptr, recs.ctypes.data, len(recs),
-                                                ctypes.cast(ctypes.pointer(b), ctypes.c_void_p), 1, 1,
-                                                status.ctypes.data, keep.ctypes.data, _lib.EB_MEM_HOST),
-                       "eb_admission_batch")
+            status, keep = admit(batch, recs)
             owner = np.repeat(np.arange(act.size), R)
             kept = keep.astype(bool) & (status == 0)
             # rank of each kept row within its instance (draw order)

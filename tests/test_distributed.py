@@ -149,3 +149,21 @@ def test_bench_max_over_ranks_gloo_world2():
     for p in procs:
         p.join(timeout=60)
     assert got == {0: 1.25, 1: 1.25}          # every rank reports the slowest rank's time
+
+
+def test_bench_self_spawns_world2_reference_arm():
+    """bench.py --gpus 2 outside torchrun re-launches itself with 2 ranks
+    (torch.distributed.run); rank 0 prints one line with n_gpus 2."""
+    import json
+    import subprocess
+    import sys
+    from helpers import ROOT
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+                          "--steps", "1", "--warmup", "0", "--n-inst", "3000", "--cpu-sample", "40"],
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["impl"] == "reference" and j["value"] > 0
+    assert j["c_port_agrees_with_reference"] is True
