@@ -291,6 +291,11 @@ int32_t eb_exhaustive_level_range(eb_handle *h, const eb_context *ctx,
  * return -1 for them. */
 int32_t eb_exhaustive_live_levels(eb_handle *h, const eb_context *ctx, int32_t k,
                                   const eb_requests *req, uint64_t *live_mask);
+/* Evidence counters of the brute-force kernels on this handle since its
+ * creation: out[0] = combinations checked with the full check_direct,
+ * out[1] = prefixes whose whole subtree the branch and bound skipped.
+ * Synchronizes the handle's stream.  No reference counterpart. */
+int32_t eb_exhaustive_counters(eb_handle *h, int64_t *out);
 
 /* ---- K2: batched feasibility / cost ----------------------------------- */
 /* check_direct(subset, ctx, padded_len) feasibility.py:192-223 for n_sub

@@ -63,6 +63,8 @@ def load():
         lib.oracle_nob.restype = None
         lib.oracle_nob.argtypes = [P, I32, P, P, P, F64, F64, I32, P, P, P, P]
         lib.oracle_admission_batch.restype = I32
+        lib.oracle_exhaustive_mt.restype = I32
+        lib.oracle_exhaustive_mt.argtypes = [P, I32, P, P, P, P, P, P, P, I32, I32, P, P, P]
         lib.oracle_admission_batch.argtypes = [P, I32, P, I32, I32, P, P, I32]
         _o = lib
     return _o
@@ -177,3 +179,39 @@ def admission_batch(batch: InstanceBatch, accuracy_check=True, prefilter=True, t
 def admit(batch: InstanceBatch, recs):
     """synth.generate's admission hook computed by the oracle (no device)."""
     return admission_batch(batch)
+
+
+def exhaustive_mt(ctx_rec, cols, threads=None, z_top=0):
+    """Literal multi-threaded level scan (no bounds, no pruning) of
+    exhaustive_optimal(mode='subsets') on a whole pool: (status, z, lexrank, checked).
+    ``z_top`` > 0 starts at that level (the caller proved the ones above infeasible)."""
+    lib = load()
+    a = {k: np.ascontiguousarray(v) for k, v in cols.items()}
+    n = int(a["prompt_tokens"].shape[0])
+    z = C.c_int32(0); rk = C.c_int64(0); chk = C.c_int64(0)
+    st = lib.oracle_exhaustive_mt(ctx_rec.ctypes.data, n, a["id"].ctypes.data, a["prompt_tokens"].ctypes.data,
+                                  a["output_tokens"].ctypes.data, a["deadline_s"].ctypes.data,
+                                  a["waiting_s"].ctypes.data, a["channel_gain"].ctypes.data,
+                                  a["uplink_power_w"].ctypes.data, int(threads or os.cpu_count() or 1),
+                                  int(z_top), C.byref(z), C.byref(rk), C.byref(chk))
+    return st, z.value, rk.value, chk.value
+
+
+def link_fractions(ctx_rec, cols):
+    """Per-member (uplink, downlink) fraction terms s*k_up and n*k_down, as
+    check_direct forms them (feasibility.py:203-205), from the oracle's libm
+    log2 -- for the tests' level-bound proofs."""
+    import math
+    r = ctx_rec[0]
+    nu = float(r["noise_density_w_hz"]) * float(r["uplink_band_hz"])
+    nd = float(r["noise_density_w_hz"]) * float(r["downlink_band_hz"])
+    up, dn = [], []
+    for s, o, g, p in zip(cols["prompt_tokens"].tolist(), cols["output_tokens"].tolist(),
+                          cols["channel_gain"].tolist(), cols["uplink_power_w"].tolist()):
+        ku = float(r["bits_per_token"]) / (float(r["uplink_slot_s"]) * float(r["uplink_band_hz"]) *
+                                          math.log2(1.0 + p * g / nu))
+        kd = float(r["bits_per_token"]) / (float(r["downlink_slot_s"]) * float(r["downlink_band_hz"]) *
+                                          math.log2(1.0 + float(r["downlink_power_w"]) * g / nd))
+        up.append(s * ku)
+        dn.append(o * kd)
+    return np.array(up), np.array(dn)

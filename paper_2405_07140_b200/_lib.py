@@ -122,6 +122,7 @@ _SIGS = {
     "eb_exhaustive_batch": (I32, [P, P, I32, P, I32, P, P, P, P, P, I32]),
     "eb_exhaustive_level_range": (I32, [P, P, I32, P, I32, I64, I64, P]),
     "eb_exhaustive_live_levels": (I32, [P, P, I32, P, P]),
+    "eb_exhaustive_counters": (I32, [P, P]),
     "eb_check_direct_batch": (I32, [P, P, I32, P, I64, I64, P, P, P, P, P, P, P, I32]),
     "eb_check_knapsack_batch": (I32, [P, I64, P, P, P, P, P, P, P, P, P, I32]),
     "eb_coefficients_batch": (I32, [P, P, I32, P, P, P, P, P, P, I32]),

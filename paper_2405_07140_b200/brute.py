@@ -106,6 +106,15 @@ def device_level_range(ctx_rec: np.ndarray, cols: dict, device=None):
     return level
 
 
+def enum_stats(device=None) -> np.ndarray:
+    """[combinations checked, prefixes pruned] by this process's brute-force
+    kernels on `device` so far (eb_exhaustive_counters)."""
+    h = _lib.handle(device)
+    out = np.zeros(2, np.int64)
+    _lib.check(h.lib.eb_exhaustive_counters(h.ptr, out.ctypes.data), "eb_exhaustive_counters")
+    return out
+
+
 def local_search(n: int, world: int, rank: int, level) -> tuple:
     """This rank's best (z, r) over its shard of every level, searching z = n..1."""
     for z in range(n, 0, -1):

@@ -5,13 +5,16 @@
 // returns the first subset that passes check_direct.  Equivalently: the
 // largest z with any feasible subset, and within it the smallest
 // lexicographic rank; nodes_visited is then
-// sum_{z'>z} C(K,z') + rank + 1.  On the device every thread owns a chunk of
-// consecutive ranks of one level, unranks its first combination once, then
-// walks lexicographic successors keeping prefix sums per position, so each
-// subset costs O(positions changed) instead of O(z) -- while every sum is
-// still the left-to-right fold check_direct computes (prefix sums of the same
-// sequence ARE the same fold).  A block-level (batch kernel) or grid-level
-// (range kernel) atomicMin keeps the first feasible rank.
+// sum_{z'>z} C(K,z') + rank + 1.  On the device threads take chunks of
+// consecutive ranks of one level from a work counter (shared memory in the
+// batch kernel, global in the range kernel), unrank a chunk's first
+// combination once, then walk lexicographic successors with branch and bound
+// over prefixes; the folds of the first z-1 members stay in registers across
+// the common last-position step, so a subset costs O(1) there while every
+// sum is still the left-to-right fold check_direct computes.  A block-level
+// (batch kernel) or grid-level (range kernel) atomicMin keeps the first
+// feasible rank.  Threads count checked combinations and pruned prefixes into
+// the handle's counters (eb_exhaustive_counters).
 #include <climits>
 
 #include "eb_internal.cuh"
@@ -240,25 +243,38 @@ __device__ __forceinline__ bool prefix_infeasible(const Members& S, int z, int p
 // when a prefix idx[0..q] cannot be completed (prefix_infeasible), the whole
 // rank range of its completions -- C(n - idx[q] - 1, z - q - 1) ranks, all
 // infeasible -- is skipped, so the first feasible rank is unchanged.
+//
+// Per-thread state is the combination idx[] (one byte per position, L1
+// resident) plus the folds of its first z-1 members in registers.  A
+// successor that changes only the last position (the common step) reuses
+// them; one that changes position j < z-1 refolds positions 0..z-2 from
+// scratch -- the same left-to-right sums check_direct computes, so every
+// value is bit-identical to a fold kept per position, without per-position
+// stacks (which spilled 2.2 KB per thread to DRAM).
+struct ScanCounters {
+  unsigned long long leaves;    // combinations checked with the full check_direct
+  unsigned long long pruned;    // prefixes cut by prefix_infeasible (whole subtrees skipped)
+};
+
 __device__ int64_t scan_chunk(const Members& S, int z, int64_t r_lo, int64_t r_hi,
-                              const unsigned long long* stop) {
+                              const unsigned long long* stop, ScanCounters& cnt) {
   const int n = S.n;
-  uint8_t idx[EB_MAX_K], tight[EB_MAX_K + 1];
-  double pu[EB_MAX_K + 1], pd[EB_MAX_K + 1];
-  int64_t ps[EB_MAX_K + 1], pf[EB_MAX_K + 1];
-  // unrank r_lo
+  uint8_t idx[EB_MAX_K];
   {
     uint64_t r = (uint64_t)r_lo;
     int v = 0;
     for (int j = 0; j < z; ++j) {
       for (;;) {
-        uint64_t cnt = binom(n - v - 1, z - j - 1);
-        if (r < cnt) { idx[j] = (uint8_t)v; ++v; break; }
-        r -= cnt; ++v;
+        uint64_t c = binom(n - v - 1, z - j - 1);
+        if (r < c) { idx[j] = (uint8_t)v; ++v; break; }
+        r -= c; ++v;
       }
     }
   }
-  pu[0] = 0.0; pd[0] = 0.0; ps[0] = 0; pf[0] = 0;
+  double cu = 0.0, cd = 0.0;      // folds of positions 0..z-2 (valid when `cached`)
+  int64_t cs = 0, cf = 0;
+  int ct = 0;
+  bool cached = false;
   int from = 0;
   bool first = true;     // r_lo may sit inside a subtree: no skipping on it
   int64_t rank = r_lo;
@@ -266,25 +282,34 @@ __device__ int64_t scan_chunk(const Members& S, int z, int64_t r_lo, int64_t r_h
   while (rank < r_hi) {
     int q = z - 1;       // subtree to leave: the full combination (1 rank)
     bool dead = false;
-    for (int j = from; j < z; ++j) {
-      const int i = idx[j];
-      pu[j + 1] = add(pu[j], S.a[i]);
-      pd[j + 1] = add(pd[j], S.b[i]);
-      ps[j + 1] = ps[j] + S.nout[i];
-      pf[j + 1] = pf[j] + S.far[i];
-      int t = i;
-      if (j > 0) {
-        const int o = tight[j];
-        if (sub(S.dl[o], S.ws[o]) <= sub(S.dl[i], S.ws[i])) t = o;
+    if (!cached || from < z - 1) {
+      double pu = 0.0, pd = 0.0;
+      int64_t ps = 0, pf = 0;
+      int t = idx[0];
+      for (int j = 0; j < z - 1; ++j) {
+        const int i = idx[j];
+        pu = add(pu, S.a[i]);
+        pd = add(pd, S.b[i]);
+        ps += S.nout[i];
+        pf += S.far[i];
+        if (j > 0 && !(sub(S.dl[t], S.ws[t]) <= sub(S.dl[i], S.ws[i]))) t = i;
+        if (j >= from && !first && prefix_infeasible(S, z, j + 1, pu, pd, ps, pf, t)) {
+          q = j;
+          dead = true;
+          break;
+        }
       }
-      tight[j + 1] = (uint8_t)t;
-      if (!first && j + 1 < z && prefix_infeasible(S, z, j + 1, pu[j + 1], pd[j + 1], ps[j + 1], pf[j + 1], t)) {
-        q = j;
-        dead = true;
-        break;
-      }
+      cached = !dead;
+      cu = pu; cd = pd; cs = ps; cf = pf; ct = t;
     }
-    if (!dead && feasible(S, z, idx, pu[z], pd[z], ps[z], pf[z])) return rank;
+    if (dead) {
+      ++cnt.pruned;
+    } else {
+      const int i = idx[z - 1];
+      ++cnt.leaves;
+      (void)ct;
+      if (feasible(S, z, idx, add(cu, S.a[i]), add(cd, S.b[i]), cs + S.nout[i], cf + S.far[i])) return rank;
+    }
     first = false;
     rank += (int64_t)binom(n - idx[q] - 1, z - q - 1);
     if ((++steps & 127) == 0 && *(volatile const unsigned long long*)stop < (unsigned long long)rank) return -1;
@@ -297,6 +322,12 @@ __device__ int64_t scan_chunk(const Members& S, int z, int64_t r_lo, int64_t r_h
     from = j;
   }
   return -1;
+}
+
+__device__ __forceinline__ void flush_counters(const ScanCounters& c, unsigned long long* stats) {
+  if (!stats) return;
+  if (c.leaves) atomicAdd(&stats[0], c.leaves);
+  if (c.pruned) atomicAdd(&stats[1], c.pruned);
 }
 
 struct BatchArgs {
@@ -313,12 +344,31 @@ struct BatchArgs {
   int64_t* lexrank;
   int64_t* nodes;
   uint64_t* mask;
+  unsigned long long* stats;   // [leaves checked, prefixes pruned] (handle counters)
 };
 
-// One block per instance (many small instances).
+__device__ uint64_t unrank_mask(int n, int z, uint64_t r) {
+  uint64_t m = 0;
+  int v = 0;
+  for (int j = 0; j < z; ++j)
+    for (;;) {
+      uint64_t cnt = binom(n - v - 1, z - j - 1);
+      if (r < cnt) { m |= 1ULL << v; ++v; break; }
+      r -= cnt; ++v;
+    }
+  return m;
+}
+
+// One block per instance (many small instances).  Each live level's rank
+// range is cut into chunks that the threads take in rank order from a shared
+// counter (no static split: a thread that finishes early takes the next
+// chunk), and every thread stops once a rank below its chunk is known
+// feasible; one barrier per level decides it.
 __global__ void __launch_bounds__(256) exh_batch_kernel(const __grid_constant__ BatchArgs A) {
   __shared__ Members S;
   __shared__ unsigned long long best;
+  __shared__ unsigned long long next;
+  ScanCounters cnt{0ULL, 0ULL};
   for (int64_t inst = blockIdx.x; inst < A.n_inst; inst += gridDim.x) {
     int64_t row0 = A.offsets[inst];
     int n = (int)(A.offsets[inst + 1] - row0);
@@ -350,14 +400,17 @@ __global__ void __launch_bounds__(256) exh_batch_kernel(const __grid_constant__ 
     for (int z = n; z >= 1; --z) {
       uint64_t total = binom(n, z);
       if (level_infeasible(S, z)) { skipped += (int64_t)total; continue; }   // block-uniform
-      if (tid0) best = ULLONG_MAX;
+      if (tid0) { best = ULLONG_MAX; next = 0ULL; }
       __syncthreads();
-      uint64_t per = (total + blockDim.x - 1) / blockDim.x;
-      uint64_t lo = per * threadIdx.x;
-      uint64_t hi = lo + per < total ? lo + per : total;
-      if (lo < hi) {
-        int64_t r = scan_chunk(S, z, (int64_t)lo, (int64_t)hi, &best);
-        if (r >= 0) atomicMin(&best, (unsigned long long)r);
+      // ~8 chunks per thread, at least 32 ranks each
+      uint64_t per = total / (8ULL * blockDim.x) + 1;
+      if (per < 32) per = 32;
+      for (;;) {
+        const uint64_t lo = atomicAdd(&next, per);
+        if (lo >= total || lo > *(volatile unsigned long long*)&best) break;
+        const uint64_t hi = lo + per < total ? lo + per : total;
+        int64_t r = scan_chunk(S, z, (int64_t)lo, (int64_t)hi, &best, cnt);
+        if (r >= 0) { atomicMin(&best, (unsigned long long)r); break; }
       }
       __syncthreads();
       unsigned long long b = best;
@@ -370,23 +423,11 @@ __global__ void __launch_bounds__(256) exh_batch_kernel(const __grid_constant__ 
       A.z_found[inst] = zf;
       A.lexrank[inst] = rk;
       A.nodes[inst] = zf ? skipped + rk + 1 : skipped;   // 2^n - 1 when none
-      if (A.mask) {
-        uint64_t m = 0;
-        if (zf) {
-          uint64_t r = (uint64_t)rk;
-          int v = 0;
-          for (int j = 0; j < zf; ++j)
-            for (;;) {
-              uint64_t cnt = binom(n - v - 1, zf - j - 1);
-              if (r < cnt) { m |= 1ULL << v; ++v; break; }
-              r -= cnt; ++v;
-            }
-        }
-        A.mask[inst] = m;
-      }
+      if (A.mask) A.mask[inst] = zf ? unrank_mask(n, zf, (uint64_t)rk) : 0ULL;
     }
     __syncthreads();
   }
+  flush_counters(cnt, A.stats);
 }
 
 struct RangeArgs {
@@ -394,11 +435,13 @@ struct RangeArgs {
   eb_requests req;
   int n, z;
   int64_t lo, hi, per;
-  unsigned long long* best;
+  unsigned long long* best;    // [0] first feasible rank, [1] next chunk (grid work counter)
   int* status;
+  unsigned long long* stats;
 };
 
-// Grid-wide: one level, rank range [lo, hi) split in chunks of `per`.
+// Grid-wide: one level, rank range [lo, hi) in chunks of `per` that the
+// threads take in rank order from a global counter.
 __global__ void __launch_bounds__(256) exh_range_kernel(const __grid_constant__ RangeArgs A) {
   __shared__ Members S;
   load_members(S, A.c, A.req, 0, A.n);
@@ -407,15 +450,18 @@ __global__ void __launch_bounds__(256) exh_range_kernel(const __grid_constant__ 
     return;
   }
   if (level_infeasible(S, A.z)) return;     // no size-z subset can be feasible
-  int64_t nchunks = (A.hi - A.lo + A.per - 1) / A.per;
-  for (int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks;
-       ch += (int64_t)gridDim.x * blockDim.x) {
-    int64_t lo = A.lo + ch * A.per;
+  const unsigned long long span = (unsigned long long)(A.hi - A.lo);
+  ScanCounters cnt{0ULL, 0ULL};
+  for (;;) {
+    const unsigned long long off = atomicAdd(&A.best[1], (unsigned long long)A.per);
+    if (off >= span) break;
+    const int64_t lo = A.lo + (int64_t)off;
     if ((unsigned long long)lo > *(volatile unsigned long long*)A.best) break;
-    int64_t hi = lo + A.per < A.hi ? lo + A.per : A.hi;
-    int64_t r = scan_chunk(S, A.z, lo, hi, A.best);
-    if (r >= 0) atomicMin(A.best, (unsigned long long)r);
+    const int64_t hi = lo + A.per < A.hi ? lo + A.per : A.hi;
+    int64_t r = scan_chunk(S, A.z, lo, hi, A.best, cnt);
+    if (r >= 0) { atomicMin(A.best, (unsigned long long)r); break; }
   }
+  flush_counters(cnt, A.stats);
 }
 
 // One block: the level bounds of one instance as a bit mask (bit z-1 = level
@@ -445,7 +491,8 @@ int launch_exh_batch(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, in
                      const eb_requests& d_req, int cap, int32_t* d_status, int32_t* d_z,
                      int64_t* d_rank, int64_t* d_nodes, uint64_t* d_mask) {
   if (n_inst <= 0) return EB_OK;
-  BatchArgs A{d_ctxs, n_ctx, n_inst, d_off, d_ci, req_base, d_req, cap, d_status, d_z, d_rank, d_nodes, d_mask};
+  BatchArgs A{d_ctxs, n_ctx, n_inst, d_off, d_ci, req_base, d_req, cap, d_status, d_z, d_rank, d_nodes, d_mask,
+              exh_stats(h)};
   int64_t grid = n_inst < (int64_t)h->num_sms * 8 ? n_inst : (int64_t)h->num_sms * 8;
   exh_batch_kernel<<<(unsigned)grid, 256, 0, st>>>(A);
   EB_CUDA(cudaGetLastError());
@@ -462,6 +509,7 @@ int exh_levels(eb_handle* h, cudaStream_t st, const eb_context& ctx_host, const 
   RangeArgs A;
   fill_ctx(A.c, ctx_host);
   A.req = d_req; A.n = n; A.z = 0; A.lo = A.hi = 0; A.per = 1; A.best = d_mask; A.status = d_status;
+  A.stats = nullptr;
   int zero = 0;
   EB_CUDA(cudaMemcpyAsync(d_status, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
   exh_levels_kernel<<<1, 256, 0, st>>>(A, d_mask);
@@ -481,20 +529,21 @@ int exh_range(eb_handle* h, cudaStream_t st, const eb_context& ctx_host, const e
   RangeArgs A;
   fill_ctx(A.c, ctx_host);
   A.req = d_req; A.n = n; A.z = z; A.lo = lo; A.hi = hi;
-  int64_t span = hi - lo;
-  int threads = 256;
-  int64_t max_threads = (int64_t)h->num_sms * 8 * threads;
-  int64_t per = (span + max_threads - 1) / max_threads;
+  const int64_t span = hi - lo;
+  const int threads = 256;
+  const int64_t max_threads = (int64_t)h->num_sms * 8 * threads;
+  // ~8 chunks per resident thread (dynamic: early finishers take more), >= 64 ranks each
+  int64_t per = span / (max_threads * 8) + 1;
   if (per < 64) per = 64;
   A.per = per;
-  A.best = d_best; A.status = d_status;
-  int64_t nchunks = (span + per - 1) / per;
+  A.best = d_best; A.status = d_status; A.stats = exh_stats(h);
+  const int64_t nchunks = (span + per - 1) / per;
   int64_t grid = (nchunks + threads - 1) / threads;
   if (grid > (int64_t)h->num_sms * 8) grid = (int64_t)h->num_sms * 8;
   if (grid < 1) grid = 1;
-  unsigned long long init = ULLONG_MAX;
+  const unsigned long long init[2] = {ULLONG_MAX, 0ULL};
   int zero = 0;
-  EB_CUDA(cudaMemcpyAsync(d_best, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+  EB_CUDA(cudaMemcpyAsync(d_best, init, sizeof(init), cudaMemcpyHostToDevice, st));
   EB_CUDA(cudaMemcpyAsync(d_status, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
   exh_range_kernel<<<(unsigned)grid, threads, 0, st>>>(A);
   EB_CUDA(cudaGetLastError());

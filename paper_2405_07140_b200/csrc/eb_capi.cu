@@ -511,6 +511,8 @@ int32_t eb_handle_create(int32_t device, eb_handle** out) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
+  EB_CUDA(cudaMalloc(&h->exh_stats, 2 * sizeof(unsigned long long)));
+  EB_CUDA(cudaMemsetAsync(h->exh_stats, 0, 2 * sizeof(unsigned long long), h->stream));
   int st = binom_init(h->stream);
   if (st) { delete h; return st; }
   EB_CUDA(cudaStreamSynchronize(h->stream));
@@ -529,6 +531,7 @@ int32_t eb_handle_destroy(eb_handle* h) {
   for (int i = 0; i < 64; ++i) cudaEventDestroy(h->cev[i]);
   if (h->in_arena) cudaFree(h->in_arena);
   if (h->dscratch) cudaFree(h->dscratch);
+  if (h->exh_stats) cudaFree(h->exh_stats);
   if (h->pinned) cudaFreeHost(h->pinned);
   for (int i = 0; i < 3; ++i) {
     if (h->ctab[i]) cudaFree(h->ctab[i]);
@@ -556,6 +559,17 @@ int32_t eb_synchronize(eb_handle* h) {
 }
 
 int64_t eb_kernel_launches(eb_handle* h) { return h ? h->launches : -1; }
+
+int32_t eb_exhaustive_counters(eb_handle* h, int64_t* out) {
+  if (!h || !out) return EB_ERR_INVALID_ARG;
+  EB_CUDA(cudaSetDevice(h->device));
+  unsigned long long v[2];
+  EB_CUDA(cudaMemcpyAsync(v, h->exh_stats, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
+  EB_CUDA(cudaStreamSynchronize(h->stream));
+  out[0] = (int64_t)v[0];
+  out[1] = (int64_t)v[1];
+  return EB_OK;
+}
 
 // ---------------------------------------------------------------------------
 int32_t eb_dftsp_batch(eb_handle* h, const eb_context* ctxs, int32_t n_ctx, const eb_search_params* prm,
@@ -714,7 +728,7 @@ int32_t eb_exhaustive_level_range(eb_handle* h, const eb_context* ctx, int32_t k
   if (rank_hi == rank_lo) return EB_OK;
   Stage S(h, h->stream);
   eb_requests d_req = upload_req(S, *req, 0, k);
-  unsigned long long* d_best = S.alloc<unsigned long long>(1);
+  unsigned long long* d_best = S.alloc<unsigned long long>(2);   // best rank, work counter
   int* d_status = S.alloc<int>(1);
   if (S.err) return S.err;
   int status = 0;

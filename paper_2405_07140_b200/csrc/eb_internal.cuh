@@ -104,9 +104,13 @@ struct eb_handle {
   // inputs of every chunk of a call (uploads never wait for a buffer to free)
   void* in_arena;
   size_t in_arena_bytes;
+  // brute-force evidence counters [combinations checked, prefixes pruned]
+  // (eb_exhaustive_counters), device memory, zeroed at handle creation
+  unsigned long long* exh_stats;
 };
 
 namespace eb {
+inline unsigned long long* exh_stats(eb_handle* h) { return h->exh_stats; }
 void set_error(const char* fmt, ...);
 int cuda_fail(cudaError_t e, const char* what);
 int ensure_dscratch(eb_handle* h, size_t bytes);

@@ -159,3 +159,57 @@ def generate(w: Workload, n_inst: int, seed: int = 2405_07140, chunk: int = 100_
             rate[act] = np.maximum(kept_per / np.maximum(R, 1), 0.02)
     offsets = np.arange(n_inst + 1, dtype=np.int64) * K
     return InstanceBatch(offsets, out, recs, prof, K)
+
+
+def brute_family(K: int, n: int, seed: int = 2405_07140, z0: int | None = None, deadline_frac: float = 0.3):
+    """Config-4 instances that keep the brute force honest: pools of K users
+    whose uplink and downlink fractions are anti-correlated (long prompts with
+    short outputs and vice versa, Rayleigh gains), with the uplink and
+    downlink slots scaled per pool so that the z0 smallest uplink terms and the
+    z0 smallest downlink terms each just fit (z0 = K/2 by default).  The level
+    bounds (z smallest terms of each resource apart) then leave every level up
+    to z0 live, while the largest jointly feasible batch is smaller: the
+    levels in between must be enumerated.  A share `deadline_frac` of the
+    users carry deadlines that only fit batches up to a per-user size, so the
+    deadline constraint binds on some subsets too.  No slot cap; memory slack.
+
+    Returns [(ctx_rec (1 record), columns)] -- the reference's
+    exhaustive_optimal(pool, ctx, cap=K) inputs."""
+    from .costs import flops_autoregressive, flops_initial
+    rng = np.random.default_rng(seed)
+    llm = get_model("bloom-3b")
+    q = get_profile("w8a16")
+    z0 = z0 or K // 2
+    out = []
+    for _ in range(n):
+        s = rng.integers(32, 2049, size=K).astype(np.int32)
+        nout = np.clip(np.rint((2 ** 21) / s * rng.uniform(0.6, 1.4, size=K)), 16, 2048).astype(np.int32)
+        gain = rng.exponential(1e-3, size=K)
+        p_up = dbm(20.0)
+        rec = contexts(Workload("brute", profiles=("w8a16",)))
+        r = rec[0]
+        noise = r["noise_density_w_hz"] * r["uplink_band_hz"]
+        eff_up = np.log2(1.0 + p_up * gain / noise)
+        eff_dn = np.log2(1.0 + r["downlink_power_w"] * gain / noise)
+        c_up = s * 16.0 / (r["uplink_band_hz"] * eff_up)           # a_i = c_up / T_up
+        c_dn = nout * 16.0 / (r["downlink_band_hz"] * eff_dn)
+        r["uplink_slot_s"] = np.sort(c_up)[:z0].sum() / 0.999
+        r["downlink_slot_s"] = np.sort(c_dn)[:z0].sum() / 0.999
+        r["has_slot_cap"] = 0
+        r["memory_bytes"] = 1e15
+        r["flops_per_s"] = 20 * 1.33e12
+        slots = float(r["uplink_slot_s"] + r["downlink_slot_s"])
+        waiting = rng.uniform(0.0, 0.5, size=K)
+        pad = int(s.max())
+        fi = flops_initial(llm, pad)
+        med = int(np.median(nout))
+        zi = rng.integers(max(1, K // 4), K + 1, size=K)
+        comp = np.array([q.beta * (int(z) * fi + int(z) * flops_autoregressive(llm, pad, med)) / r["flops_per_s"]
+                         for z in zi])
+        tight = rng.random(K) < deadline_frac
+        deadline = np.where(tight, waiting + slots + comp, waiting + slots + 1e3)
+        cols = {"id": np.arange(K, dtype=np.int64), "prompt_tokens": s, "output_tokens": nout,
+                "deadline_s": deadline.astype(np.float64), "waiting_s": waiting, "tolerance": np.ones(K),
+                "channel_gain": gain, "uplink_power_w": np.full(K, p_up)}
+        out.append((rec, {k: np.ascontiguousarray(v) for k, v in cols.items()}))
+    return out
