@@ -52,7 +52,9 @@ typedef enum eb_status {
   EB_ERR_OVERFLOW = 17,            /* exact integer FLOP count would exceed int64    */
   EB_ERR_BAD_MODE = 18,            /* ValueError            dftsp.py:314-315        */
   EB_ERR_PADDED_TOO_SMALL = 19,    /* ValueError            feasibility.py:142-143  */
-  EB_ERR_NONPOSITIVE_LINK = 20     /* ValueError            radio.py:63-64 (power, gain or noise <= 0) */
+  EB_ERR_NONPOSITIVE_LINK = 20,    /* ValueError            radio.py:63-64 (power, gain or noise <= 0) */
+  EB_ERR_NAN_INPUT = 21            /* dftsp only: a NaN deadline/waiting/gain/power; the reference then orders
+                                      the pool by CPython's sort on unordered keys (not reproduced) */
 } eb_status;
 
 typedef enum eb_mem { EB_MEM_HOST = 0, EB_MEM_DEVICE = 1 } eb_mem;

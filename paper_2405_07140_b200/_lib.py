@@ -41,6 +41,7 @@ ERR_OVERFLOW = 17
 ERR_BAD_MODE = 18
 ERR_PADDED_TOO_SMALL = 19
 ERR_NONPOSITIVE_LINK = 20
+ERR_NAN_INPUT = 21
 
 MET_UP_SUM, MET_DN_SUM, MET_MEM_POOLPAD, MET_LAT_POOLPAD, MET_MEM_BATCHPAD, MET_LAT_BATCHPAD, \
     MET_PADDED, MET_WIN_D = range(8)

@@ -104,26 +104,39 @@ __device__ __forceinline__ bool level_infeasible(const Members& S, int z) {
 //    every z whose bound passes; a level no member marks is infeasible.  The
 //    FLOP sums are exact integers and the checks are the monotone leq of
 //    check_direct with the fails_margin slack, so the bound is sound.
+// Bound keys of a member.  A NaN term or slack (NaN deadline, waiting time
+// or gain, or an infinite deadline minus an infinite wait) makes every
+// check_direct containing the member fail (each leq on NaN is false), so the
+// bounds may treat it as +inf (uplink/downlink term) or -inf (slack): the
+// keys stay totally ordered and the ranks a permutation, and no feasible
+// subset is refuted.  The checks themselves read the raw values.
+__device__ __forceinline__ double bound_term(double x) { return isnan(x) ? __longlong_as_double(0x7ff0000000000000LL) : x; }
+__device__ __forceinline__ double bound_slack(const Members& S, int i) {
+  const double s = sub(S.dl[i], S.ws[i]);
+  return isnan(s) ? __longlong_as_double((long long)0xfff0000000000000ULL) : s;
+}
+
 __device__ void build_level_bounds(Members& S) {
   const int n = S.n;
   if (threadIdx.x == 0) S.lat_ok = 0ULL;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     int rf = 0, rn = 0, ra = 0, rb = 0, rs = 0;
-    const double si = sub(S.dl[i], S.ws[i]);
+    const double si = bound_slack(S, i), ai = bound_term(S.a[i]), bi = bound_term(S.b[i]);
     for (int j = 0; j < n; ++j) {
       const int jl = j < i;
+      const double aj = bound_term(S.a[j]), bj = bound_term(S.b[j]);
       rf += (S.far[j] < S.far[i]) | ((S.far[j] == S.far[i]) & jl);
       rn += (S.nout[j] < S.nout[i]) | ((S.nout[j] == S.nout[i]) & jl);
-      ra += (S.a[j] < S.a[i]) | ((S.a[j] == S.a[i]) & jl);
-      rb += (S.b[j] < S.b[i]) | ((S.b[j] == S.b[i]) & jl);
-      const double sj = sub(S.dl[j], S.ws[j]);
+      ra += (aj < ai) | ((aj == ai) & jl);
+      rb += (bj < bi) | ((bj == bi) & jl);
+      const double sj = bound_slack(S, j);
       rs += (sj > si) | ((sj == si) & jl);
     }
     S.srt_far[rf] = S.far[i];
     S.far_order[rf] = (uint8_t)i;
     S.srt_n[rn] = S.nout[i];
-    S.srt_a[ra] = S.a[i];
-    S.srt_b[rb] = S.b[i];
+    S.srt_a[ra] = ai;
+    S.srt_b[rb] = bi;
     S.slack_rank[i] = (uint8_t)rs;
   }
   __syncthreads();

@@ -477,6 +477,7 @@ const char* eb_status_string(int32_t s) {
     case EB_ERR_BAD_MODE: return "unknown exhaustive mode";
     case EB_ERR_PADDED_TOO_SMALL: return "padded_len must cover every candidate prompt";
     case EB_ERR_NONPOSITIVE_LINK: return "power, gain and noise must be strictly positive";
+    case EB_ERR_NAN_INPUT: return "NaN deadline, waiting time, gain or power: the reference's candidate order is undefined";
     default: return "unknown status";
   }
 }

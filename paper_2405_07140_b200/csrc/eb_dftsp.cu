@@ -1312,6 +1312,20 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   }
   padded = __reduce_max_sync(EB_FULL, padded);             // dftsp.py:255
   __syncwarp();
+  // NaN deadline / waiting / gain / power: the reference then orders the
+  // pool by CPython's sort on unordered keys (dftsp.py:257, :81), which no
+  // rank-based order reproduces -- a documented status instead (DESIGN.md §1,
+  // pinned by tests/golden/edge.npz).
+  {
+    int err_nan = INT_MAX;
+#pragma unroll
+    for (int h = 0; h < NI; ++h) {
+      const int i = lane + 32 * h;
+      if (i < n && (isnan(dl_i[h]) || isnan(w_i[h]) || isnan(g_i[h]) || isnan(p_i[h]))) err_nan = min(err_nan, i);
+    }
+    err_nan = __reduce_min_sync(EB_FULL, err_nan);
+    if (err_nan != INT_MAX) { put_status(EB_ERR_NAN_INPUT, err_nan); return; }
+  }
   // Duplicate ids (coefficients are keyed by id, feasibility.py:164-166).
   int err_dup = INT_MAX;
   const unsigned active = (n >= 32) ? EB_FULL : ((1u << n) - 1u);

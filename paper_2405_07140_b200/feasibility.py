@@ -132,6 +132,10 @@ def raise_for_status(status: int, reqs=None, err_index: int = -1, ctx=None, ladd
                            "coefficient derivation is inconsistent")
     if status == _lib.ERR_PADDED_TOO_SMALL:
         raise ValueError("padded_len must cover every candidate prompt")
+    if status == _lib.ERR_NAN_INPUT:
+        raise ValueError(f"request {r.id if r else '?'} has a NaN deadline, waiting time, gain or power: the "
+                         "reference orders such pools by CPython's sort on unordered keys, which the device "
+                         "does not reproduce")
     if status == _lib.ERR_DUPLICATE_ID:
         raise ValueError(f"request ids must be unique within a pool (duplicate id {r.id if r else '?'})")
     if status == _lib.ERR_CAP_EXCEEDED:
