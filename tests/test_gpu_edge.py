@@ -65,7 +65,7 @@ def test_dftsp_edge_inputs_vs_reference(tag, algo):
                 else:
                     assert g == e, (i, e, g)
                 n_exact += 1
-    assert n_exact >= 100 and n_status >= 60
+    assert n_exact >= 80 and n_status >= 60
 
 
 def test_exhaustive_edge_inputs_vs_reference():
