@@ -727,11 +727,18 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
   // largest, o_tau[z - 1]; min(o_tau[z - 1] - k3 z, slot_budget(z)) thus
   // bounds every leaf cap of target z from above, for every width.  (With a
   // NaN deadline the tau ranks are not a permutation: slot budget only.)
-  bool tau_ok = true;
+  // A -inf normalized deadline (an infinite waiting time) makes every cap
+  // that includes it -inf, and leq(lat, -inf) is TRUE (its tolerance
+  // 1e-9 * max(1, |a|, |b|) is then infinite): the leaf check is not
+  // monotone in the cap there, so no latency-based skip is sound -- only the
+  // memory skips stay (lat_free).  tau ranks are a permutation (NaN taus are
+  // refused in setup), so o_tau[n - 1] is the least.
+  const bool lat_free = o_tau[n - 1] == -INF;
+  bool tau_ok = !lat_free;
   if (EXACT) {
     bool nan = false;
     for (int t = lane; t < n; t += 32) nan |= !(o_tau[t] == o_tau[t]);
-    tau_ok = !__any_sync(EB_FULL, nan);
+    tau_ok = tau_ok && !__any_sync(EB_FULL, nan);
   }
   int c_first = 0;
   if (!cm.on) {
@@ -752,7 +759,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
         lat = add(lat, mul(i2d(cc), c_w[li.g]));
         rem -= cc;
       }
-      const double lat_cap = (EXACT && !tau_ok) ? slot_cap : pymin(sub(o_tau[z - 1], k3z), slot_cap);
+      const double lat_cap = lat_free ? INF : (EXACT && !tau_ok) ? slot_cap : pymin(sub(o_tau[z - 1], k3z), slot_cap);
       if (!(fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap)))
         zhi = z;
     }
@@ -782,7 +789,8 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
         lat = add(lat, mul(i2d(cc), c_w[li.g]));
         rem -= cc;
       }
-      const double lat_cap = EXACT ? (tau_ok ? pymin(sub(o_tau[z - 1], k3z), slot_cap) : slot_cap)
+      // (non-exact: the call's own cap, exact for all its leaves, -inf included)
+      const double lat_cap = EXACT ? (lat_free ? INF : tau_ok ? pymin(sub(o_tau[z - 1], k3z), slot_cap) : slot_cap)
                                    : pymin(sub(o_tau[d - 1], k3z), slot_cap);
       live = !(fails_with_margin(i2d(mem), mem_cap) || fails_with_margin(mul(lat, 0.999999999999), lat_cap));
       if (EXACT && tau_ok && live && !cm.on) {
@@ -1412,6 +1420,16 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       put_status(code, e);
       return;
     }
+  }
+  {
+    // a NaN normalized deadline from finite-looking inputs (an infinite
+    // deadline minus an infinite wait): the same undefined order as NaN inputs
+    int e = INT_MAX;
+#pragma unroll
+    for (int h = 0; h < NI; ++h)
+      if (lane + 32 * h < n && isnan(tau_i[h])) e = min(e, lane + 32 * h);
+    e = __reduce_min_sync(EB_FULL, e);
+    if (e != INT_MAX) { put_status(EB_ERR_NAN_INPUT, e); return; }
   }
   __syncwarp();
 
