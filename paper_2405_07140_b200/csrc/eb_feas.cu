@@ -16,32 +16,71 @@ __device__ __forceinline__ int ctx_at(const int32_t* idx, int64_t i, int n_ctx) 
 }
 
 // ---- link math radio.py:64-101 ------------------------------------------
-__global__ void link_kernel(const eb_context* ctxs, int n_ctx, eb_requests req, int64_t n,
-                            const int32_t* req_ctx, int32_t* status, double* out) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    int ci = ctx_at(req_ctx, j, n_ctx);
-    double* o = out + 6 * j;
-    if (ci < 0) { status[j] = EB_ERR_INVALID_ARG; continue; }
-    const Ctx c = load_ctx(&ctxs[ci]);
-    double g = req.channel_gain[j], pu = req.uplink_power_w[j];
-    int st = 0;
-    double eu = 0.0, ed = 0.0, ku = 0.0, kd = 0.0;
-    // radio.py:63-64: nonpositive power/gain/noise raise before log2
-    if (pu <= 0.0 || g <= 0.0 || c.N0_up <= 0.0) st = EB_ERR_NONPOSITIVE_LINK;
-    else {
-      eu = spectral_efficiency(pu, g, c.N0_up);
-      if (eu <= 0.0) st = EB_ERR_UPLINK_EFF_ZERO; else ku = fraction_per_token(c.fbits, c.T_up, c.B_up, eu);
+// Block-strided tiles of 128 requests: the SoA columns are read coalesced (one
+// element per thread), the six results of each request are staged in shared
+// memory column-major ([field][request], conflict-free writes), and the tile's
+// 6 x 128 doubles -- contiguous in the ABI's row-major out[j*6 + k] -- leave as
+// coalesced 16-byte stores (the ragged last tile element-wise).
+constexpr int kLinkTile = 128;
+
+__global__ void __launch_bounds__(kLinkTile) link_kernel(const eb_context* ctxs, int n_ctx, eb_requests req,
+                                                         int64_t n, const int32_t* req_ctx, int32_t* status,
+                                                         double* out) {
+  __shared__ double tile[6][kLinkTile + 1];
+  for (int64_t t0 = (int64_t)blockIdx.x * kLinkTile; t0 < n; t0 += (int64_t)gridDim.x * kLinkTile) {
+    const int64_t j = t0 + threadIdx.x;
+    const int rows = (int)min((int64_t)kLinkTile, n - t0);
+    double o[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    bool write = false;
+    if (j < n) {
+      const int ci = ctx_at(req_ctx, j, n_ctx);
+      if (ci < 0) {
+        status[j] = EB_ERR_INVALID_ARG;     // row left untouched, as before
+      } else {
+        const Ctx c = load_ctx(&ctxs[ci]);
+        const double g = req.channel_gain[j], pu = req.uplink_power_w[j];
+        int st = 0;
+        double eu = 0.0, ed = 0.0, ku = 0.0, kd = 0.0;
+        // radio.py:63-64: nonpositive power/gain/noise raise before log2
+        if (pu <= 0.0 || g <= 0.0 || c.N0_up <= 0.0) st = EB_ERR_NONPOSITIVE_LINK;
+        else {
+          eu = spectral_efficiency(pu, g, c.N0_up);
+          if (eu <= 0.0) st = EB_ERR_UPLINK_EFF_ZERO; else ku = fraction_per_token(c.fbits, c.T_up, c.B_up, eu);
+        }
+        if (c.P_dn <= 0.0 || g <= 0.0 || c.N0_dn <= 0.0) { if (!st) st = EB_ERR_NONPOSITIVE_LINK; }
+        else {
+          ed = spectral_efficiency(c.P_dn, g, c.N0_dn);
+          if (ed <= 0.0) { if (!st) st = EB_ERR_DOWNLINK_EFF_ZERO; } else kd = fraction_per_token(c.fbits, c.T_dn, c.B_dn, ed);
+        }
+        o[0] = eu; o[1] = ed; o[2] = ku; o[3] = kd;
+        o[4] = mul(i2d(req.prompt_tokens[j]), ku);   // min_uplink_fraction radio.py:87-94
+        o[5] = mul(i2d(req.output_tokens[j]), kd);   // min_downlink_fraction radio.py:97-101
+        status[j] = st;
+        write = true;
+      }
     }
-    if (c.P_dn <= 0.0 || g <= 0.0 || c.N0_dn <= 0.0) { if (!st) st = EB_ERR_NONPOSITIVE_LINK; }
-    else {
-      ed = spectral_efficiency(c.P_dn, g, c.N0_dn);
-      if (ed <= 0.0) { if (!st) st = EB_ERR_DOWNLINK_EFF_ZERO; } else kd = fraction_per_token(c.fbits, c.T_dn, c.B_dn, ed);
+    const bool all = __syncthreads_and(write || j >= n) && rows == kLinkTile;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) tile[k][threadIdx.x] = o[k];
+    __syncthreads();
+    double* base = out + 6 * t0;
+    if (all && ((uintptr_t)base & 15) == 0) {
+      // 3 x 128 double2 stores cover the tile; pair q holds flat values 2q, 2q+1
+      double2* b2 = reinterpret_cast<double2*>(base);
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const int q = r * kLinkTile + threadIdx.x;
+        const int f0 = 2 * q, f1 = 2 * q + 1;
+        b2[q] = make_double2(tile[f0 % 6][f0 / 6], tile[f1 % 6][f1 / 6]);
+      }
+    } else {
+      for (int f = threadIdx.x; f < 6 * rows; f += kLinkTile) {
+        const int r = f / 6;
+        if (req_ctx && ctx_at(req_ctx, t0 + r, n_ctx) < 0) continue;   // invalid rows stay untouched
+        base[f] = tile[f % 6][r];
+      }
     }
-    o[0] = eu; o[1] = ed; o[2] = ku; o[3] = kd;
-    o[4] = mul(i2d(req.prompt_tokens[j]), ku);   // min_uplink_fraction radio.py:87-94
-    o[5] = mul(i2d(req.output_tokens[j]), kd);   // min_downlink_fraction radio.py:97-101
-    status[j] = st;
+    __syncthreads();
   }
 }
 
@@ -351,7 +390,7 @@ inline unsigned grid_for(eb_handle* h, int64_t n, int threads) {
 int launch_link(eb_handle* h, cudaStream_t st, const eb_context* ctxs, int n_ctx, const eb_requests& req,
                 int64_t n, const int32_t* req_ctx, int32_t* status, double* out) {
   if (n <= 0) return EB_OK;
-  link_kernel<<<grid_for(h, n, 128), 128, 0, st>>>(ctxs, n_ctx, req, n, req_ctx, status, out);
+  link_kernel<<<grid_for(h, n, kLinkTile), kLinkTile, 0, st>>>(ctxs, n_ctx, req, n, req_ctx, status, out);
   EB_LAUNCHED();
   return EB_OK;
 }
