@@ -89,46 +89,67 @@ __global__ void coeff_kernel(const eb_context* ctxs, int n_ctx, int64_t n_inst, 
                              const int32_t* ctx_index, int64_t req_base, eb_requests req,
                              const int64_t* padded_len, int32_t* status, int32_t* err_index,
                              double* out_scalar, double* out_req) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_inst;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int ci = ctx_at(ctx_index, i, n_ctx);
-    if (ci < 0) { status[i] = EB_ERR_INVALID_ARG; continue; }
+  // one warp per instance, lanes over its rows (coalesced SoA loads); the
+  // reference's sequential scans become ballots for the first offending row
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_inst; i += warps) {
+    const int ci = ctx_at(ctx_index, i, n_ctx);
+    if (ci < 0) { if (lane == 0) status[i] = EB_ERR_INVALID_ARG; continue; }
     const Ctx c = load_ctx(&ctxs[ci]);
-    int64_t lo = off[i] - req_base, hi = off[i + 1] - req_base;
+    const int64_t lo = off[i] - req_base, hi = off[i + 1] - req_base;
     int64_t padded = padded_len ? padded_len[i] : 0;
-    if (padded <= 0) {
-      padded = 0;
-      for (int64_t r = lo; r < hi; ++r) padded = max(padded, (int64_t)req.prompt_tokens[r]);
-    }
     int st = 0, err = -1;
-    for (int64_t r = lo; r < hi && !st; ++r)
-      if (req.prompt_tokens[r] > padded) { st = EB_ERR_PADDED_TOO_SMALL; err = (int)(r - lo); }
-    int64_t m1 = weight_bytes(c.m);
-    double headroom = sub(div(c.M, c.alpha), i2d(m1));
-    if (!st && headroom < 0) st = EB_ERR_WEIGHTS_DO_NOT_FIT;
-    double* sc = out_scalar + 6 * i;
-    if (!st) {
-      int64_t kv = kv_per_token(c.m);
-      int64_t gb = gen_base(c.m, padded);
-      sc[0] = div(headroom, i2d(kv));
-      sc[1] = i2d(flops_initial(c.m, padded) - c.m.L * gb);
-      sc[2] = i2d(c.m.L * (gb - 2 * c.m.d));
-      sc[3] = i2d(2 * c.m.L * c.m.d);
-      sc[4] = c.has_cap ? div(mul(c.cap_s, c.C), c.beta) : __longlong_as_double(0x7ff8000000000000LL);
-      sc[5] = (double)padded;
-      for (int64_t r = lo; r < hi; ++r) {
-        double ku = 0.0, kd = 0.0;
-        int s2 = k_up_of(c, req.channel_gain[r], req.uplink_power_w[r], &ku);
-        if (!s2) s2 = k_dn_of(c, req.channel_gain[r], &kd);
-        if (s2) { st = s2; err = (int)(r - lo); break; }
-        double* o = out_req + 4 * r;
-        o[0] = ku; o[1] = kd;
-        o[2] = tau_base_of(c, req.deadline_s[r], req.waiting_s[r]);
-        o[3] = mul(i2d(req.prompt_tokens[r]), ku);
+    if (padded <= 0) {
+      int m = 0;
+      for (int64_t r = lo + lane; r < hi; r += 32) m = max(m, req.prompt_tokens[r]);
+      padded = (int64_t)__reduce_max_sync(EB_FULL, m);
+    } else {
+      for (int64_t r0 = lo; r0 < hi && !st; r0 += 32) {                 // feasibility.py:142-143
+        const int64_t r = r0 + lane;
+        const unsigned bad = __ballot_sync(EB_FULL, r < hi && req.prompt_tokens[r] > padded);
+        if (bad) { st = EB_ERR_PADDED_TOO_SMALL; err = (int)(r0 - lo) + __ffs(bad) - 1; }
       }
     }
-    status[i] = st;
-    if (err_index) err_index[i] = err;
+    const int64_t m1 = weight_bytes(c.m);
+    const double headroom = sub(div(c.M, c.alpha), i2d(m1));
+    if (!st && headroom < 0) st = EB_ERR_WEIGHTS_DO_NOT_FIT;
+    if (!st) {
+      if (lane == 0) {
+        double* sc = out_scalar + 6 * i;
+        const int64_t kv = kv_per_token(c.m);
+        const int64_t gb = gen_base(c.m, padded);
+        sc[0] = div(headroom, i2d(kv));
+        sc[1] = i2d(flops_initial(c.m, padded) - c.m.L * gb);
+        sc[2] = i2d(c.m.L * (gb - 2 * c.m.d));
+        sc[3] = i2d(2 * c.m.L * c.m.d);
+        sc[4] = c.has_cap ? div(mul(c.cap_s, c.C), c.beta) : __longlong_as_double(0x7ff8000000000000LL);
+        sc[5] = (double)padded;
+      }
+      // feasibility.py:164-166 in pool order: rows before the first link error are written
+      for (int64_t r0 = lo; r0 < hi; r0 += 32) {
+        const int64_t r = r0 + lane;
+        double ku = 0.0, kd = 0.0;
+        int s2 = 0;
+        if (r < hi) {
+          s2 = k_up_of(c, req.channel_gain[r], req.uplink_power_w[r], &ku);
+          if (!s2) s2 = k_dn_of(c, req.channel_gain[r], &kd);
+        }
+        const unsigned bad = __ballot_sync(EB_FULL, s2 != 0);
+        const int first = bad ? __ffs(bad) - 1 : 32;
+        if (r < hi && lane < first) {
+          double* o = out_req + 4 * r;
+          o[0] = ku; o[1] = kd;
+          o[2] = tau_base_of(c, req.deadline_s[r], req.waiting_s[r]);
+          o[3] = mul(i2d(req.prompt_tokens[r]), ku);
+        }
+        if (bad) { st = __shfl_sync(EB_FULL, s2, first); err = (int)(r0 - lo) + first; break; }
+      }
+    }
+    if (lane == 0) {
+      status[i] = st;
+      if (err_index) err_index[i] = err;
+    }
   }
 }
 
@@ -217,33 +238,64 @@ __global__ void check_knapsack_kernel(int64_t n_sub, const int64_t* sub_off, con
 }
 
 // sim._dftsp_candidates sim.py:264-274 (accuracy filter + alone prefilter).
-__global__ void admission_kernel(const eb_context* ctxs, int n_ctx, int64_t n_inst, const int64_t* off,
-                                 const int32_t* ctx_index, int64_t req_base, eb_requests req,
-                                 int acc_check, int prefilter, int32_t* status, uint8_t* keep) {
-  // grid-stride over rows; the instance of a row is found by binary search.
-  int64_t n_rows = off[n_inst] - off[0];
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n_rows;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    int64_t row = off[0] + q;
-    int64_t lo = 0, hi = n_inst;   // find i with off[i] <= row < off[i+1]
-    while (hi - lo > 1) { int64_t mid = (lo + hi) >> 1; if (off[mid] <= row) lo = mid; else hi = mid; }
-    int ci = ctx_at(ctx_index, lo, n_ctx);
-    int64_t r = row - req_base;
-    if (ci < 0) { status[r] = EB_ERR_INVALID_ARG; keep[r] = 0; continue; }
-    const Ctx c = load_ctx(&ctxs[ci]);
-    int st = 0;
-    bool k = true;
-    if (acc_check) {
-      double tol = req.tolerance[r];
-      if (c.delta < 0 || tol < 0) { st = EB_ERR_INVALID_ARG; k = false; }   // catalog.py:153-154
-      else k = c.delta <= tol;                                              // catalog.py:155
+__global__ void __launch_bounds__(128) admission_kernel(const eb_context* ctxs, int n_ctx, int64_t n_inst,
+                                                        const int64_t* off, const int32_t* ctx_index,
+                                                        int64_t req_base, eb_requests req, int acc_check,
+                                                        int prefilter, int32_t* status, uint8_t* keep) {
+  // Tiles of 128 rows; the instance of a row is found by binary search in a
+  // shared-memory window of the offsets (one global search per tile for its
+  // first row), so the per-row search does not chase dependent global loads.
+  constexpr int W = 128;
+  __shared__ int64_t win[W + 1];
+  __shared__ int64_t s_i0;
+  const int64_t n_rows = off[n_inst] - off[0];
+  for (int64_t t0 = (int64_t)blockIdx.x * W; t0 < n_rows; t0 += (int64_t)gridDim.x * W) {
+    if (threadIdx.x == 0) {
+      const int64_t row = off[0] + t0;
+      int64_t lo = 0, hi = n_inst;   // off[lo] <= row < off[lo + 1]
+      while (hi - lo > 1) { int64_t mid = (lo + hi) >> 1; if (off[mid] <= row) lo = mid; else hi = mid; }
+      s_i0 = lo;
     }
-    if (k && prefilter) {
-      int res = check_direct_rows(c, req, 1, [&](int) { return r; }, (int64_t)req.prompt_tokens[r], nullptr);
-      if (res < 0) { st = -res; k = false; } else k = res > 0;
+    __syncthreads();
+    const int64_t i0 = s_i0;
+    for (int k = threadIdx.x; k <= W; k += blockDim.x) win[k] = (i0 + k <= n_inst) ? off[i0 + k] : INT64_MAX;
+    __syncthreads();
+    const int64_t q = t0 + threadIdx.x;
+    if (q < n_rows) {
+      const int64_t row = off[0] + q;
+      int64_t inst;
+      if (row < win[W]) {
+        int a = 0, b = W;            // win[a] <= row < win[a + 1]
+        while (b - a > 1) { const int mid = (a + b) >> 1; if (win[mid] <= row) a = mid; else b = mid; }
+        inst = i0 + a;
+      } else {                       // more than W (empty) instances in the tile
+        int64_t lo = i0 + W, hi = n_inst;
+        while (hi - lo > 1) { int64_t mid = (lo + hi) >> 1; if (off[mid] <= row) lo = mid; else hi = mid; }
+        inst = lo;
+      }
+      const int ci = ctx_at(ctx_index, inst, n_ctx);
+      const int64_t r = row - req_base;
+      if (ci < 0) {
+        status[r] = EB_ERR_INVALID_ARG;
+        keep[r] = 0;
+      } else {
+        const Ctx c = load_ctx(&ctxs[ci]);
+        int st = 0;
+        bool k = true;
+        if (acc_check) {
+          const double tol = req.tolerance[r];
+          if (c.delta < 0 || tol < 0) { st = EB_ERR_INVALID_ARG; k = false; }   // catalog.py:153-154
+          else k = c.delta <= tol;                                              // catalog.py:155
+        }
+        if (k && prefilter) {
+          const int res = check_direct_rows(c, req, 1, [&](int) { return r; }, (int64_t)req.prompt_tokens[r], nullptr);
+          if (res < 0) { st = -res; k = false; } else k = res > 0;
+        }
+        status[r] = st;
+        keep[r] = k;
+      }
     }
-    status[r] = st;
-    keep[r] = k;
+    __syncthreads();
   }
 }
 
@@ -398,7 +450,7 @@ int launch_coeff(eb_handle* h, cudaStream_t st, const eb_context* ctxs, int n_ct
                  const int64_t* off, const int32_t* ci, int64_t req_base, const eb_requests& req,
                  const int64_t* padded, int32_t* status, int32_t* err, double* sc, double* rq) {
   if (n_inst <= 0) return EB_OK;
-  coeff_kernel<<<grid_for(h, n_inst, 128), 128, 0, st>>>(ctxs, n_ctx, n_inst, off, ci, req_base, req, padded,
+  coeff_kernel<<<grid_for(h, n_inst * 32, 128), 128, 0, st>>>(ctxs, n_ctx, n_inst, off, ci, req_base, req, padded,
                                                         status, err, sc, rq);
   EB_LAUNCHED();
   return EB_OK;
