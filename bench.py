@@ -217,10 +217,11 @@ class ClockSampler:
                 "window": "timed region" if in_window else "warm-up and timed region"}
 
 
-def ncu_profile():
-    """The committed ncu capture of the search kernel, and whether it was taken on these sources."""
+def ncu_profile(config: int = 2):
+    """The committed ncu capture of this config's search kernel, and whether it was taken on these sources."""
+    name = "ncu_config5_summary.json" if config == 5 else "ncu_dftsp_summary.json"
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_dftsp_summary.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
             j = json.load(fh)
     except (OSError, ValueError):
         return None, False
@@ -534,7 +535,7 @@ def run_dftsp(args, world, rank, local):
     per_launch_s = dev_s / args.steps
     achieved = ops_per_inst * n / per_launch_s / 1e12
     peak = fp64_peak.value / 1e12
-    prof, current = ncu_profile()
+    prof, current = ncu_profile(args.config)
     issue = {"peak_measured": round(issue_peak.value / 1e9, 1),
              "peak_nominal": round(props.multi_processor_count * 4 * f_mhz * 1e6 / 1e9, 1), "unit": "G warp-inst/s"}
     traffic = None
@@ -555,10 +556,11 @@ def run_dftsp(args, world, rank, local):
     if not args.no_cpu and world == 1:
         import pyref
         if pyref.available():
-            per = args.cpu_sample or threads * 40
-            rate, _, t, agree = reference_rate(batch, ladder, per, 3, 1, threads)
+            per = args.cpu_sample or threads * 250      # ~1 s of the 16-core box per step, ~10 s in all
+            reps = 10
+            rate, _, t, agree = reference_rate(batch, ladder, per, reps, 1, threads)
             cpu = {"value": round(rate, 2), "unit": "instances/s", "cores": threads, "kind": "reference",
-                   "sample": f"3 x {per} instances of this workload, unmodified Python reference edgebatch.dftsp "
+                   "sample": f"{reps} x {per} instances of this workload, unmodified Python reference edgebatch.dftsp "
                              f"(oracle/_ref) in ProcessPoolExecutor({threads}), {t:.1f} s",
                    "c_port_agrees_with_reference": agree}
         else:

@@ -14,7 +14,9 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libedgebatch_b200.so")
+# EB_LIB_PATH: an alternative build of the same library (tools/variants.sh
+# launch-bound experiments); the default is the in-tree build
+LIB_PATH = os.environ.get("EB_LIB_PATH") or os.path.join(HERE, "libedgebatch_b200.so")
 
 ABI_VERSION = 2        # include/edgebatch_b200.h EB_ABI_VERSION
 EB_MAX_K = 64

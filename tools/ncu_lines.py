@@ -8,7 +8,12 @@ import sys
 
 def load(path):
     rows, f, hdr = [], None, None
-    for r in csv.reader(open(path)):
+    if path.endswith(".gz"):
+        import gzip
+        fh = gzip.open(path, "rt")
+    else:
+        fh = open(path)
+    for r in csv.reader(fh):
         if not r:
             continue
         if r[0] == "File Path":

@@ -2,7 +2,7 @@
 """Summarise an ncu --set full report (one kernel launch) into the JSON kept
 under profiles/: duration, DRAM bytes, warp instructions, issue activity,
 occupancy, registers, stall breakdown.  Usage:
-  tools/ncu_summary.py REPORT.ncu-rep KERNEL_REGEX UNITS_PER_LAUNCH [--launch i]"""
+  tools/ncu_summary.py REPORT.ncu-rep|RAW.csv KERNEL_REGEX UNITS_PER_LAUNCH [--launch i]"""
 import csv
 import io
 import json
@@ -33,10 +33,17 @@ STALLS = ["barrier", "branch_resolving", "dispatch_stall", "long_scoreboard", "m
 def main():
     rep, kern, units = sys.argv[1], sys.argv[2], float(sys.argv[3])
     launch = int(sys.argv[sys.argv.index("--launch") + 1]) if "--launch" in sys.argv else 0
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base", "-k", f"regex:{kern}"],
-                         capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
-    hdr, data = rows[0], rows[2:]
+    if rep.endswith(".csv"):      # a `--page raw --csv --print-units base` export (tools/evidence_pass.sh)
+        import re
+        rows = list(csv.reader(open(rep)))
+        hdr = rows[0]
+        kn = hdr.index("Kernel Name")
+        data = [r for r in rows[2:] if re.search(kern, r[kn])]
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base", "-k",
+                              f"regex:{kern}"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        hdr, data = rows[0], rows[2:]
     row = dict(zip(hdr, data[launch]))
 
     def val(name):
