@@ -292,6 +292,13 @@ __device__ __forceinline__ int dfs_step(Lane& s, const Tables& T) {
 //    a margin far beyond floating-point error cannot contain a passing leaf
 //    and is skipped without enumeration (its node counts are still added).
 // ===========================================================================
+// Exact warp sum of int64 values (butterfly; every lane gets the total).
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(EB_FULL, v, o);
+  return v;
+}
+
 __device__ __forceinline__ bool fails_with_margin(double a_lo, double b) {
   // true only if leq(a, b) is false for every a >= a_lo (leq is monotone in a)
   const double m = fmax(fmax(1.0, fabs_(a_lo)), fabs_(b));
@@ -1304,6 +1311,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
 #pragma unroll
   for (int h = 0; h < NI; ++h) {
     int i = lane + 32 * h;
+    id_i[h] = 0;
     if (i < n) {
       int64_t r = r0 + i;
       s_i[h] = A.req.prompt_tokens[r];
@@ -1360,6 +1368,22 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   }
   err_dup = __reduce_min_sync(EB_FULL, err_dup);
   if (err_dup != INT_MAX) { put_status(EB_ERR_DUPLICATE_ID, err_dup); return; }
+  // ids rising along the rows (the common layout): the solution's id order
+  // is then its row order (finish)
+  bool ids_rise;
+  {
+    bool rise = true;
+#pragma unroll
+    for (int h = 0; h < NI; ++h) {
+      int64_t nx = __shfl_down_sync(EB_FULL, id_i[h], 1);
+      if (h + 1 < NI) {
+        const int64_t nx2 = __shfl_sync(EB_FULL, id_i[h + 1 < NI ? h + 1 : h], 0);
+        if (lane == 31) nx = nx2;
+      }
+      if (lane + 32 * h + 1 < n) rise &= id_i[h] < nx;
+    }
+    ids_rise = __all_sync(EB_FULL, rise);
+  }
 
   // The exact integer cost model runs in int64: refuse instances whose
   // FLOP / byte counts could leave its range (double estimate, 4x margin).
@@ -1438,8 +1462,12 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   int t_i[NI], gcls_i[NI], kr_i[NI];
   bool first_i[NI];
   unsigned peers = 0;     // NI == 1: lanes with my output length
+  unsigned tau_ties = 0;  // NI == 1: other lanes with my tau
   if constexpr (NI == 1) {
     peers = __match_any_sync(EB_FULL, lane < n ? len_i[0] : -1) & active;
+    const double tz = tau_i[0] == 0.0 ? 0.0 : tau_i[0];
+    tau_ties = __match_any_sync(EB_FULL, lane < n ? (unsigned long long)__double_as_longlong(tz) : ~0ULL) & active &
+               ~(1u << lane);
   }
 #pragma unroll
   for (int h = 0; h < NI; ++h) {
@@ -1450,10 +1478,11 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       int t = 0;
       bool first = true;
       if constexpr (NI == 1) {
-        for (int j = 0; j < n; ++j) {
-          double tj = a_tau[j];
-          t += (int)(tj > tau_i[h]) | ((int)(tj == tau_i[h]) & (int)(a_id[j] < id_i[h]));
-        }
+        // tau rank: requests with a larger tau, then equal-tau requests with a
+        // smaller id (lanes holding the same tau, by a match; -0.0 is
+        // folded onto +0.0 so that equal doubles match)
+#pragma unroll 4
+        for (int j = 0; j < n; ++j) t += (int)(a_tau[j] > tau_i[h]);
         first = (peers & lanemask_lt()) == 0;
       } else {
         // one branch-free pass: tau rank, class leadership, within-class rank
@@ -1469,6 +1498,8 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
         first = !earlier;
         kr_i[h] = kr;
       }
+      if constexpr (NI == 1)
+        for (unsigned m = tau_ties; m; m &= m - 1) t += (int)(a_id[__ffs(m) - 1] < id_i[h]);
       t_i[h] = t;
       first_i[h] = first;
     }
@@ -1491,7 +1522,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       if (i < n) {
         bool ok = false;
 #pragma unroll
-        for (int q = 0; q < EB_MAX_CLASSES; ++q) ok |= (q < A.prm.ladder_len) & (A.prm.ladder[q] == len_i[h]);
+        for (int q = 0; q < A.prm.ladder_len; ++q) ok |= A.prm.ladder[q] == len_i[h];
         if (!ok && t_i[h] < bad_t) { bad_t = t_i[h]; bad_i = i; }
       }
     }
@@ -1505,6 +1536,12 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       return;
     }
   }
+  unsigned key_ties = 0;   // NI == 1: other lanes with my key (within-class order ties)
+  if constexpr (NI == 1) {
+    const double kz = key_i[0] == 0.0 ? 0.0 : key_i[0];
+    key_ties = __match_any_sync(EB_FULL, lane < n ? (unsigned long long)__double_as_longlong(kz) : ~0ULL) & active &
+               ~(1u << lane);
+  }
 #pragma unroll
   for (int h = 0; h < NI; ++h) {
     int i = lane + 32 * h;
@@ -1513,11 +1550,8 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       if constexpr (NI == 1) {
         // class index: class leaders with a shorter output; rank among peers
         for (unsigned fm = fmask[0]; fm; fm &= fm - 1) g += a_len[__ffs(fm) - 1] < len_i[h];
-        for (unsigned pm = peers & ~(1u << lane); pm; pm &= pm - 1) {
-          const int j = __ffs(pm) - 1;
-          const double kj = a_key[j];
-          kr += (int)(kj < key_i[h]) | ((int)(kj == key_i[h]) & (int)(a_id[j] < id_i[h]));
-        }
+        for (unsigned pm = peers & ~(1u << lane); pm; pm &= pm - 1) kr += (int)(a_key[__ffs(pm) - 1] < key_i[h]);
+        for (unsigned pm = peers & key_ties; pm; pm &= pm - 1) kr += (int)(a_id[__ffs(pm) - 1] < id_i[h]);
       } else {
         // class index: leaders with a shorter output (kr came with the ranks)
 #pragma unroll
@@ -1596,8 +1630,14 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     int base = (d - 1) * d / 2 + (d - 1) * Gi;
     int k = 0, start = 0;
     LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
+    // level of the class the d-th request (tau order) joined: the count
+    // recurrence of width d differs from width d-1 only at that level and
+    // above (row[0].pad[0]; meaningful when the class count is unchanged)
+    const int gn = o_g[d - 1];
+    int kn = 0;
     for (int g = 0; g < Gi; ++g) {
       int sz = sizes[(d - 1) * Gi + g];
+      if (g == gn) kn = k;
       if (sz > 0) {
         LevelInfo li;
         li.off = (uint16_t)(base + start);
@@ -1612,12 +1652,6 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     ncls_d[d - 1] = (uint8_t)k;
     int tail = 0;
     for (int q = k - 1; q >= 0; --q) { row[q].tail_next = (uint8_t)tail; tail += row[q].size; }
-    // level of the class the d-th request (tau order) joined: the count
-    // recurrence of width d differs from width d-1 only at that level and
-    // above (row[0].pad[0]; meaningful when the class count is unchanged)
-    const int gn = o_g[d - 1];
-    int kn = 0;
-    for (int q = 0; q < k; ++q) if (row[q].g == gn) kn = q;
     row[0].pad[0] = (uint8_t)kn;
   }
   if constexpr (ALGO == 1) {
@@ -1816,80 +1850,109 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       }
     }
     __syncwarp();
-    // integer sums are order-free: lanes over members, then warp reductions
-    int64_t sn = 0, fl_pool = 0, fl_batch = 0;
+    // Lanes = member slots j = lane + 32 h of the subset (recover order).
+    // Integer sums are order-free: sum_j flops_autoregressive(s, n_j) =
+    // L * (base(s) * S1 + 2 d * S2) with S1 = sum (n_j - 1), S2 = sum
+    // (n_j - 1) n_j -- the same integers as the per-member closed forms, so
+    // one pair of reductions serves both paddings.
+    int t_m[NI], loc_m[NI];
+    double key_m[NI], dnt_m[NI];
+    int64_t s1 = 0, s2 = 0;
     int pb = 0;
-    for (int j = lane; j < zf; j += 32) {
-      const int t = sol[j];
-      sn += o_len[t];
-      pb = max(pb, o_s[t]);
-      fl_pool += flops_autoregressive(C.m, padded, o_len[t]);
-    }
-    // the batch-padding cost (sim.py:372-376) only feeds the optional metrics
-    const bool want_met = O.metrics != nullptr;
-    if (want_met) {
-      pb = __reduce_max_sync(EB_FULL, pb);
-      for (int j = lane; j < zf; j += 32) fl_batch += flops_autoregressive(C.m, pb, o_len[sol[j]]);
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sn += __shfl_xor_sync(EB_FULL, sn, o);
-      fl_pool += __shfl_xor_sync(EB_FULL, fl_pool, o);
-      if (want_met) fl_batch += __shfl_xor_sync(EB_FULL, fl_batch, o);
+    for (int h = 0; h < NI; ++h) {
+      const int j = lane + 32 * h;
+      t_m[h] = 0;
+      loc_m[h] = -1;
+      key_m[h] = dnt_m[h] = 0.0;
+      if (j < zf) {
+        const int t = sol[j];
+        const int64_t ln = o_len[t];
+        t_m[h] = t;
+        loc_m[h] = o_local[t];
+        key_m[h] = o_key[t];
+        dnt_m[h] = o_dnt[t];
+        s1 += ln - 1;
+        s2 += (ln - 1) * ln;
+        pb = max(pb, o_s[t]);
+      }
     }
-    fl_pool += (int64_t)zf * fi_pad;                                   // z * flops_initial + sum(...)
+    s1 = warp_sum_i64(s1);
+    s2 = warp_sum_i64(s2);
+    const int64_t sn = s1 + zf;                                        // sum of output tokens
+    const int64_t fl_pool = (int64_t)zf * fi_pad + C.m.L * (gen_base(C.m, padded) * s1 + 2 * C.m.d * s2);
     const double compute_s = compute_seconds(C, fl_pool);
     bool late = false;                                                 // per-member deadline checks
-    for (int j = lane; j < zf; j += 32) late |= !leq(add(o_ws[sol[j]], compute_s), o_dl[sol[j]]);
+#pragma unroll
+    for (int h = 0; h < NI; ++h)
+      if (lane + 32 * h < zf) late |= !leq(add(o_ws[t_m[h]], compute_s), o_dl[t_m[h]]);
     late = __any_sync(EB_FULL, late);
-    if (lane == 0) {
-      double up = 0.0, dn = 0.0;                                       // folds in subset order
-      for (int j = 0; j < zf; ++j) {
-        const int t = sol[j];
-        up = add(up, o_key[t]);      // r.prompt_tokens * k_up
-        dn = add(dn, o_dnt[t]);      // r.output_tokens * k_down
-      }
-      int64_t mem = m1 + kv * (int64_t)padded * zf;
-      mem += kv * sn;
-      bool ok = leq(up, 1.0) && leq(dn, 1.0) && leq(mul(C.alpha, i2d(mem)), C.M);
-      if (ok && C.has_cap) ok = leq(compute_s, C.cap_s);
-      if (ok && late) ok = false;
-      if (!ok) status = EB_ERR_REVERIFY;
-      if (want_met) {
-        // batch_cost at the batch's own padding (sim.py:372-376)
-        int64_t mem_b = m1 + kv * (int64_t)pb * zf + kv * sn;
-        fl_batch += (int64_t)zf * flops_initial(C.m, pb);
-        met[EB_MET_UP_SUM] = up;
-        met[EB_MET_DN_SUM] = dn;
-        met[EB_MET_MEM_POOLPAD] = mul(C.alpha, i2d(mem));
-        met[EB_MET_LAT_POOLPAD] = compute_s;
-        met[EB_MET_MEM_BATCHPAD] = mul(C.alpha, i2d(mem_b));
-        met[EB_MET_LAT_BATCHPAD] = compute_seconds(C, fl_batch);
-        met[EB_MET_WIN_D] = (double)dwin;
+    // check_direct's folds in subset order (feasibility.py:203-205): every
+    // lane runs the same left fold over the members' registers
+    double up = 0.0, dn = 0.0;
+#pragma unroll
+    for (int h = 0; h < NI; ++h) {
+      const int zh = min(zf - 32 * h, 32);
+      for (int j = 0; j < zh; ++j) {
+        up = add(up, __shfl_sync(EB_FULL, key_m[h], j));     // r.prompt_tokens * k_up
+        dn = add(dn, __shfl_sync(EB_FULL, dnt_m[h], j));     // r.output_tokens * k_down
       }
     }
-    status = __shfl_sync(EB_FULL, status, 0);
-    __syncwarp();
+    const int64_t mem = m1 + kv * (int64_t)padded * zf + kv * sn;
+    bool ok = leq(up, 1.0) && leq(dn, 1.0) && leq(mul(C.alpha, i2d(mem)), C.M);
+    if (ok && C.has_cap) ok = leq(compute_s, C.cap_s);
+    if (ok && late) ok = false;
+    if (!ok) status = EB_ERR_REVERIFY;
+    if (O.metrics) {
+      // batch_cost at the batch's own padding (sim.py:372-376)
+      pb = __reduce_max_sync(EB_FULL, pb);
+      const int64_t mem_b = m1 + kv * (int64_t)pb * zf + kv * sn;
+      const int64_t fl_batch = (int64_t)zf * flops_initial(C.m, pb) + C.m.L * (gen_base(C.m, pb) * s1 + 2 * C.m.d * s2);
+      met[EB_MET_UP_SUM] = up;
+      met[EB_MET_DN_SUM] = dn;
+      met[EB_MET_MEM_POOLPAD] = mul(C.alpha, i2d(mem));
+      met[EB_MET_LAT_POOLPAD] = compute_s;
+      met[EB_MET_MEM_BATCHPAD] = mul(C.alpha, i2d(mem_b));
+      met[EB_MET_LAT_BATCHPAD] = compute_seconds(C, fl_batch);
+      met[EB_MET_WIN_D] = (double)dwin;
+    }
+    // the subset's rows as a bit set over local row positions (rows < 64)
+    uint32_t rows_lo = 0, rows_hi = 0;
+#pragma unroll
+    for (int h = 0; h < NI; ++h) {
+      const int loc = loc_m[h];
+      rows_lo |= (loc >= 0 && loc < 32) ? (1u << loc) : 0u;
+      rows_hi |= (loc >= 32 && loc < 64) ? (1u << (loc - 32)) : 0u;
+    }
+    rows_lo = __reduce_or_sync(EB_FULL, rows_lo);
+    if (NI > 1) rows_hi = __reduce_or_sync(EB_FULL, rows_hi);
     // solution sorted by request id (dftsp.py:281)
     if (status == EB_OK && O.solution) {
-      for (int j = lane; j < zf; j += 32) {
-        int t = sol[j];
-        int64_t idv = o_id[t];
-        int rank = 0;
-        for (int q = 0; q < zf; ++q) rank += o_id[sol[q]] < idv;
-        O.solution[r0 + rank] = o_local[t];
+      if (NI <= 2 && ids_rise) {
+        // ids rise along the rows: id order is row order, so a member's
+        // slot is the number of member rows before it
+#pragma unroll
+        for (int h = 0; h < NI; ++h) {
+          const int i = lane + 32 * h;
+          const uint32_t word = h ? rows_hi : rows_lo;
+          if (i < n && ((word >> lane) & 1u))
+            O.solution[r0 + (h ? __popc(rows_lo) : 0) + __popc(word & lanemask_lt())] = i;
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < NI; ++h) {
+          const int j = lane + 32 * h;
+          if (j < zf) {
+            const int64_t idv = o_id[t_m[h]];
+            int rank = 0;
+            for (int q = 0; q < zf; ++q) rank += o_id[sol[q]] < idv;
+            O.solution[r0 + rank] = loc_m[h];
+          }
+        }
       }
     }
-    if (status == EB_OK && O.solution_mask) {
-      uint64_t bits = 0;
-      for (int j = lane; j < zf; j += 32) {
-        const int loc = o_local[sol[j]];
-        if (loc < 64) bits |= 1ULL << loc;
-      }
-      bits = (uint64_t)__reduce_or_sync(EB_FULL, (unsigned)bits) |
-             ((uint64_t)__reduce_or_sync(EB_FULL, (unsigned)(bits >> 32)) << 32);
-      if (lane == 0) O.solution_mask[inst] = n <= 64 ? bits : 0ULL;
-    }
+    if (status == EB_OK && O.solution_mask && lane == 0)
+      O.solution_mask[inst] = n <= 64 ? (((uint64_t)rows_hi << 32) | rows_lo) : 0ULL;
   }
   if (O.solution_mask && lane == 0 && (!found || status != EB_OK)) O.solution_mask[inst] = 0ULL;
   // rows past the batch are unused: mark them
