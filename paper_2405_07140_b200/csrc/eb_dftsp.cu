@@ -27,6 +27,7 @@
 // count_table_kernel (node-count tables), dfs_single_kernel (one dfs call).
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 
 #include "eb_internal.cuh"
 
@@ -65,6 +66,7 @@ struct Lay {
   size_t t_up, t_dn, t_tau;                                 // prefix tables
   size_t ring_v, ring_p, ring_done, sol;
   size_t pq, pre, pf;                                       // v2: unranking / call prefix / F tables
+  size_t pm;                                                // v2, K <= 64: class-list positions per width
   size_t total;
   int T;
 };
@@ -107,8 +109,9 @@ __host__ __device__ inline Lay make_lay(int K, int G, bool exact, bool v2) {
     L.pq = take(sc);
     L.pf = L.pq;
     L.pre = take(4 * 64 + 8 * 32);
+    L.pm = K <= 64 ? take(8 * (size_t)K) : 0;
   } else {
-    L.pq = L.pre = L.pf = 0;
+    L.pq = L.pre = L.pf = L.pm = 0;
   }
   L.total = o;
   return L;
@@ -680,6 +683,9 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
   uint64_t* pre64 = (uint64_t*)(smem + L.pre + 4 * 64);
   uint64_t* pfv = (uint64_t*)(smem + L.pf);
   uint64_t* pfp = pfv + (size_t)Gi * (n + 1);
+  const uint64_t* pm = (const uint64_t*)(smem + L.pm);     // width masks (NI <= 2, setup)
+  using WMask = typename std::conditional<NI == 1, uint32_t, uint64_t>::type;
+  auto wm_ffs = [](WMask b) -> int { return NI == 1 ? __ffs((unsigned)b) - 1 : __ffsll((long long)b) - 1; };
   const int LV = Gi > 1 ? Gi - 1 : 1;
   const int W = n + 2;
 
@@ -813,12 +819,22 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
         for (int k = 0; k < m && r2 > 0; ++k) {
           const LevelInfo li = row[k];
           int lim = 0;
-          for (int p = cm.c_start[li.g], seen = 0; seen < (int)li.size && lim < r2; ++p) {
-            const int t = cm.c_list[p];
-            if (t >= d) continue;
-            ++seen;
-            if (fails_with_margin(lat_m, sub(o_tau[t], k3z))) break;
-            ++lim;
+          if constexpr (NI <= 2) {
+            WMask bits = (WMask)pm[d - 1] & ((WMask)~(WMask)0 << cm.c_start[li.g]);
+            for (int seen = 0; seen < (int)li.size && lim < r2; ++seen) {
+              const int t = cm.c_list[wm_ffs(bits)];
+              bits &= bits - 1;
+              if (fails_with_margin(lat_m, sub(o_tau[t], k3z))) break;
+              ++lim;
+            }
+          } else {
+            for (int p = cm.c_start[li.g], seen = 0; seen < (int)li.size && lim < r2; ++p) {
+              const int t = cm.c_list[p];
+              if (t >= d) continue;
+              ++seen;
+              if (fails_with_margin(lat_m, sub(o_tau[t], k3z))) break;
+              ++lim;
+            }
           }
           mem2 += (int64_t)lim * c_len[li.g];
           lat2 = add(lat2, mul(i2d(lim), c_w[li.g]));
@@ -942,13 +958,26 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
           // (dftsp.py:119-128): the same sequential folds over the class's
           // first cc members among the dd first by tau, in key order
           double cu = 0.0, cdn = 0.0, tm = INF;
-          for (int p = cm.c_start[li.g], taken = 0; taken < cc; ++p) {
-            const int t = cm.c_list[p];
-            if (t < dd) {
+          if constexpr (NI <= 2) {
+            // the class's members inside the pool, in key order: set bits of
+            // the width mask from the class start on
+            WMask bits = (WMask)pm[dd - 1] & ((WMask)~(WMask)0 << cm.c_start[li.g]);
+            for (int q = 0; q < cc; ++q) {
+              const int t = cm.c_list[wm_ffs(bits)];
+              bits &= bits - 1;
               cu = add(cu, cm.o_key[t]);
               cdn = add(cdn, cm.o_dnt[t]);
               if (EXACT) tm = pymin(tm, o_tau[t]);
-              ++taken;
+            }
+          } else {
+            for (int p = cm.c_start[li.g], taken = 0; taken < cc; ++p) {
+              const int t = cm.c_list[p];
+              if (t < dd) {
+                cu = add(cu, cm.o_key[t]);
+                cdn = add(cdn, cm.o_dnt[t]);
+                if (EXACT) tm = pymin(tm, o_tau[t]);
+                ++taken;
+              }
             }
           }
           u = add(u, cu);                                          // up_acc + up[k][x]
@@ -970,15 +999,27 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
           for (int k = 0; k < m; ++k) {
             const LevelInfo li = row[k];
             const int want = getV(V0, V1, k);
-            int taken = 0;
-            for (int p = cm.c_start[li.g]; taken < want; ++p) {
-              const int t = cm.c_list[p];
-              if (t >= dd) continue;
-              up2 = add(up2, cm.o_key[t]);                         // up += k_up * s
-              dn2 = add(dn2, cm.o_dnt[t]);                         // dn += k_down * n
-              mem2 += c_len[li.g];                                 // mem += n
-              lat2 = add(lat2, c_w[li.g]);                         // lat += latency_weight(n)
-              ++taken;
+            if constexpr (NI <= 2) {
+              WMask bits = (WMask)pm[dd - 1] & ((WMask)~(WMask)0 << cm.c_start[li.g]);
+              for (int q = 0; q < want; ++q) {
+                const int t = cm.c_list[wm_ffs(bits)];
+                bits &= bits - 1;
+                up2 = add(up2, cm.o_key[t]);                       // up += k_up * s
+                dn2 = add(dn2, cm.o_dnt[t]);                       // dn += k_down * n
+                mem2 += c_len[li.g];                               // mem += n
+                lat2 = add(lat2, c_w[li.g]);                       // lat += latency_weight(n)
+              }
+            } else {
+              int taken = 0;
+              for (int p = cm.c_start[li.g]; taken < want; ++p) {
+                const int t = cm.c_list[p];
+                if (t >= dd) continue;
+                up2 = add(up2, cm.o_key[t]);                       // up += k_up * s
+                dn2 = add(dn2, cm.o_dnt[t]);                       // dn += k_down * n
+                mem2 += c_len[li.g];                               // mem += n
+                lat2 = add(lat2, c_w[li.g]);                       // lat += latency_weight(n)
+                ++taken;
+              }
             }
           }
           const double cap2 = pymin(sub(o_tau[dd - 1], k3z), slot_cap);   // min(tau_min, slot_budget(z))
@@ -1600,6 +1641,34 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     if (i < n) c_list[c_start[gcls_i[h]] + kr_i[h]] = (uint8_t)t_i[h];
   }
   __syncwarp();
+  if constexpr (ALGO == 2 && NI <= 2) {
+    // width masks: pm[d - 1] = the class-list positions of the d first
+    // requests in tau order (an OR-scan over tau ranks), so a leaf's walk
+    // over a class visits only the members inside its pool.  `sol` is free
+    // until the finish phase: it holds each tau rank's position meanwhile.
+    uint64_t* pm = (uint64_t*)(smem + L.pm);
+#pragma unroll
+    for (int h = 0; h < NI; ++h) {
+      const int i = lane + 32 * h;
+      if (i < n) sol[t_i[h]] = (uint8_t)(c_start[gcls_i[h]] + kr_i[h]);
+    }
+    __syncwarp();
+    uint64_t carry = 0;
+#pragma unroll
+    for (int h = 0; h < NI; ++h) {
+      const int t = lane + 32 * h;
+      uint64_t v = t < n ? (1ULL << sol[t]) : 0ULL;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t u = __shfl_up_sync(EB_FULL, v, o);
+        if (lane >= o) v |= u;
+      }
+      v |= carry;
+      if (t < n) pm[t] = v;
+      carry = __shfl_sync(EB_FULL, v, 31);
+    }
+    __syncwarp();
+  }
 
   // ---------------- per pool width d: class sizes, levels, tables --------
   const int nDG = n * Gi;
