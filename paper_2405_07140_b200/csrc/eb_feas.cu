@@ -242,37 +242,43 @@ __global__ void __launch_bounds__(128) admission_kernel(const eb_context* ctxs, 
                                                         const int64_t* off, const int32_t* ctx_index,
                                                         int64_t req_base, eb_requests req, int acc_check,
                                                         int prefilter, int32_t* status, uint8_t* keep) {
-  // Tiles of 128 rows; the instance of a row is found by binary search in a
-  // shared-memory window of the offsets (one global search per tile for its
-  // first row), so the per-row search does not chase dependent global loads.
+  // Each block owns one contiguous range of rows, walked in tiles of 128.
+  // The instance of a row is found by binary search in a shared-memory
+  // window of the offsets starting at the instance of the tile's first row;
+  // that instance is carried from tile to tile (one global search per block,
+  // not per tile), so no tile waits on a chain of dependent global loads.
   constexpr int W = 128;
   __shared__ int64_t win[W + 1];
   __shared__ int64_t s_i0;
   const int64_t n_rows = off[n_inst] - off[0];
-  for (int64_t t0 = (int64_t)blockIdx.x * W; t0 < n_rows; t0 += (int64_t)gridDim.x * W) {
-    if (threadIdx.x == 0) {
-      const int64_t row = off[0] + t0;
-      int64_t lo = 0, hi = n_inst;   // off[lo] <= row < off[lo + 1]
-      while (hi - lo > 1) { int64_t mid = (lo + hi) >> 1; if (off[mid] <= row) lo = mid; else hi = mid; }
-      s_i0 = lo;
-    }
-    __syncthreads();
+  const int64_t per_blk = ((n_rows + gridDim.x - 1) / gridDim.x + W - 1) / W * W;
+  const int64_t q_lo = (int64_t)blockIdx.x * per_blk;
+  const int64_t q_hi = q_lo + per_blk < n_rows ? q_lo + per_blk : n_rows;
+  if (q_lo >= n_rows) return;
+  auto global_search = [&](int64_t row, int64_t lo) -> int64_t {   // off[lo] <= row < off[lo + 1]
+    int64_t hi = n_inst;
+    while (hi - lo > 1) { const int64_t mid = (lo + hi) >> 1; if (off[mid] <= row) lo = mid; else hi = mid; }
+    return lo;
+  };
+  if (threadIdx.x == 0) s_i0 = global_search(off[0] + q_lo, 0);
+  for (int64_t t0 = q_lo; t0 < q_hi; t0 += W) {
+    __syncthreads();                 // s_i0 is set; the previous tile is done with win
     const int64_t i0 = s_i0;
     for (int k = threadIdx.x; k <= W; k += blockDim.x) win[k] = (i0 + k <= n_inst) ? off[i0 + k] : INT64_MAX;
     __syncthreads();
-    const int64_t q = t0 + threadIdx.x;
-    if (q < n_rows) {
-      const int64_t row = off[0] + q;
-      int64_t inst;
+    auto inst_of = [&](int64_t row) -> int64_t {
       if (row < win[W]) {
         int a = 0, b = W;            // win[a] <= row < win[a + 1]
         while (b - a > 1) { const int mid = (a + b) >> 1; if (win[mid] <= row) a = mid; else b = mid; }
-        inst = i0 + a;
-      } else {                       // more than W (empty) instances in the tile
-        int64_t lo = i0 + W, hi = n_inst;
-        while (hi - lo > 1) { int64_t mid = (lo + hi) >> 1; if (off[mid] <= row) lo = mid; else hi = mid; }
-        inst = lo;
+        return i0 + a;
       }
+      return global_search(row, i0 + W);   // more than W (empty) instances in the tile
+    };
+    if (threadIdx.x == 0 && t0 + W < q_hi) s_i0 = inst_of(off[0] + t0 + W);   // next tile's first row
+    const int64_t q = t0 + threadIdx.x;
+    if (q < q_hi) {
+      const int64_t row = off[0] + q;
+      const int64_t inst = inst_of(row);
       const int ci = ctx_at(ctx_index, inst, n_ctx);
       const int64_t r = row - req_base;
       if (ci < 0) {
