@@ -53,7 +53,7 @@ struct __align__(8) LevelInfo {
   uint8_t pad[3];
 };
 
-__host__ __device__ inline size_t al8(size_t x) { return (x + 7) & ~size_t(7); }
+__host__ __device__ constexpr inline size_t al8(size_t x) { return (x + 7) & ~size_t(7); }
 
 // Per-warp shared memory layout (bytes).  K = max instance size, G = max
 // classes.  Tables hold sum_{d=1..K} (d + G) entries per array.
@@ -71,8 +71,8 @@ struct Lay {
   int T;
 };
 
-__host__ __device__ inline Lay make_lay(int K, int G, bool exact, bool v2) {
-  Lay L;
+__host__ __device__ constexpr inline Lay make_lay(int K, int G, bool exact, bool v2) {
+  Lay L{};
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = al8(o + bytes); return r; };
   L.a_tau = take(8 * K); L.a_key = take(8 * K); L.a_id = take(8 * K); L.a_len = take(4 * K);
@@ -1291,12 +1291,16 @@ __device__ __noinline__ void write_status(const eb_dftsp_result& O, int64_t inst
     for (int j = lane; j < n; j += 32) O.solution[r0 + j] = -1;
 }
 
-template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI>
+// FK > 0: the launch's layout is make_lay(FK, EB_FIXED_G, EXACT, v2), known
+// at compile time (shared-memory offsets become immediates); 0: A.lay.
+#define EB_FIXED_G 3
+template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI, int FK = 0>
 __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* smem, int& passed,
                                bool have_meta = false, int64_t m_row0 = 0, int64_t m_row1 = 0, int m_ci = 0) {
   const int lane = threadIdx.x & 31;
   const int K = A.K, G = A.G;
-  const Lay& L = A.lay;       // computed once on the host (make_lay)
+  constexpr Lay LF = make_lay(FK > 0 ? FK : 1, EB_FIXED_G, EXACT, ALGO == 2);
+  const Lay& L = FK > 0 ? LF : A.lay;       // computed once on the host (make_lay)
   double* a_tau = (double*)(smem + L.a_tau);
   double* a_key = (double*)(smem + L.a_key);
   int64_t* a_id = (int64_t*)(smem + L.a_id);
@@ -2103,12 +2107,13 @@ __global__ void __launch_bounds__(32, 1) dftsp_wide_kernel(const __grid_constant
 #ifndef EB_LOCK_MINB
 #define EB_LOCK_MINB 1
 #endif
-template <bool PRUNE, bool INCL, bool EXACT, int NI>
+template <bool PRUNE, bool INCL, bool EXACT, int NI, int FK = 0>
 __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   __shared__ int s_q[3];           // round bases, two rounds ahead (ring of 3)
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  unsigned char* smem = smem_all + warp * A.warp_bytes;
+  constexpr size_t WB = al8(make_lay(FK > 0 ? FK : 1, EB_FIXED_G, EXACT, true).total);
+  unsigned char* smem = smem_all + warp * (FK > 0 ? WB : A.warp_bytes);
   const int64_t total = A.list_count ? (int64_t)*A.list_count : A.n_inst;
   auto inst_of = [&](int64_t slot) -> int64_t { return A.inst_list ? (int64_t)A.inst_list[slot] : slot; };
   // offsets / context index of a round's instance, loaded one round early so
@@ -2134,7 +2139,7 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
     meta_of(nxt + warp, a0, a1, aci);
     const int64_t slot = base + warp;
     int passed = 0;
-    if (slot < total) solve_instance<PRUNE, INCL, EXACT, 2, NI>(A, inst_of(slot), smem, passed, true, c0, c1, cci);
+    if (slot < total) solve_instance<PRUNE, INCL, EXACT, 2, NI, FK>(A, inst_of(slot), smem, passed, true, c0, c1, cci);
     __syncwarp();
     for (; passed < 3; ++passed)
       if ((EB_LOCK_BARRIERS >> passed) & 1) __syncthreads();
@@ -2144,9 +2149,9 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
   }
 }
 
-template <bool PRUNE, bool INCL, bool EXACT, int NI>
+template <bool PRUNE, bool INCL, bool EXACT, int NI, int FK = 0>
 __global__ void __launch_bounds__(EB_LOCK_THREADS, EB_LOCK_MINB) dftsp_lock_kernel(const __grid_constant__ DftspArgs A) {
-  lock_loop<PRUNE, INCL, EXACT, NI>(A);
+  lock_loop<PRUNE, INCL, EXACT, NI, FK>(A);
 }
 
 // Wide instances (EB_MAX_K < n <= EB_MAX_K_DFTSP) with at most three classes
@@ -2397,7 +2402,10 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   }
   if (algo != 1 && al8(make_lay(K, G, exact, true).total) * 2 > smem_cap) algo = 1;
   if (algo != 1) algo = 2;
-  A.lay = make_lay(K, G, exact, algo == 2);
+  // K <= 32 with at most EB_FIXED_G classes (the paper's ladder): the
+  // leaf-parallel kernel with the layout of K = 32 compiled in
+  const bool fixed = algo == 2 && K <= 32 && G <= EB_FIXED_G;
+  A.lay = fixed ? make_lay(32, EB_FIXED_G, exact, true) : make_lay(K, G, exact, algo == 2);
   A.warp_bytes = al8(A.lay.total);
   int warps = (int)(smem_cap / A.warp_bytes);
   if (warps > 4) warps = 4;
@@ -2414,13 +2422,13 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
     else kern = exact ? dftsp_kernel<false, false, true, AL, NI> : dftsp_kernel<false, false, false, AL, NI>; \
   }
 #define EB_PICK(AL) if (K <= 32) { EB_PICK3(AL, 1) } else { EB_PICK3(AL, 2) }
-#define EB_PICKL3(NI)                                                                                  \
+#define EB_PICKL3(NI, FK)                                                                              \
   if (P) {                                                                                             \
-    if (I) kern = exact ? dftsp_lock_kernel<true, true, true, NI> : dftsp_lock_kernel<true, true, false, NI>;   \
-    else kern = exact ? dftsp_lock_kernel<true, false, true, NI> : dftsp_lock_kernel<true, false, false, NI>;   \
+    if (I) kern = exact ? dftsp_lock_kernel<true, true, true, NI, FK> : dftsp_lock_kernel<true, true, false, NI, FK>;   \
+    else kern = exact ? dftsp_lock_kernel<true, false, true, NI, FK> : dftsp_lock_kernel<true, false, false, NI, FK>;   \
   } else {                                                                                             \
-    if (I) kern = exact ? dftsp_lock_kernel<false, true, true, NI> : dftsp_lock_kernel<false, true, false, NI>; \
-    else kern = exact ? dftsp_lock_kernel<false, false, true, NI> : dftsp_lock_kernel<false, false, false, NI>; \
+    if (I) kern = exact ? dftsp_lock_kernel<false, true, true, NI, FK> : dftsp_lock_kernel<false, true, false, NI, FK>; \
+    else kern = exact ? dftsp_lock_kernel<false, false, true, NI, FK> : dftsp_lock_kernel<false, false, false, NI, FK>; \
   }
   if (algo == 2) {
     // Lockstep blocks (one instance per warp, phases shared by the block).
@@ -2432,7 +2440,7 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
     // 8-warp block.  EB_LOCK_WARPS caps the width (tuning).
     int cap_w = 8;
     if (const char* e = getenv("EB_LOCK_WARPS")) { int v = atoi(e); if (v >= 1 && v <= 16) cap_w = v; }
-    if (K <= 32) { EB_PICKL3(1) } else { EB_PICKL3(2) }
+    if (fixed) { EB_PICKL3(1, 32) } else if (K <= 32) { EB_PICKL3(1, 0) } else { EB_PICKL3(2, 0) }
     {
       struct WCache { void (*k)(DftspArgs); size_t wb; int cap; int dev; int w; };
       static thread_local WCache wc[8];
