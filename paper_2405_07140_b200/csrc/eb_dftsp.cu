@@ -1953,7 +1953,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     s1 = warp_sum_i64(s1);
     s2 = warp_sum_i64(s2);
     const int64_t sn = s1 + zf;                                        // sum of output tokens
-    const int64_t fl_pool = (int64_t)zf * fi_pad + C.m.L * (gen_base(C.m, padded) * s1 + 2 * C.m.d * s2);
+    const int64_t fl_pool = (int64_t)zf * fi_pad + C.m.L * (gb * s1 + 2 * C.m.d * s2);
     const double compute_s = compute_seconds(C, fl_pool);
     bool late = false;                                                 // per-member deadline checks
 #pragma unroll
