@@ -2158,9 +2158,21 @@ __global__ void __launch_bounds__(EB_LOCK_THREADS, EB_LOCK_MINB) dftsp_lock_kern
 // on the leaf-parallel search: up to 8 requests per lane, no unranking
 // tables (closed form), count rows past the table range; few warps per SM
 // (the per-warp footprint is O(K)), so the full register file per thread.
+// NI = 4 serves pools of at most 128 candidates with half the per-lane
+// arrays (fewer registers, more resident warps); NI = 8 the rest.
+#ifndef EB_WIDE4_THREADS
+#define EB_WIDE4_THREADS 128
+#endif
+#ifndef EB_WIDE4_MINB
+#define EB_WIDE4_MINB 3
+#endif
 template <bool PRUNE, bool INCL, bool EXACT>
 __global__ void __launch_bounds__(64, 1) dftsp_lock_wide_kernel(const __grid_constant__ DftspArgs A) {
   lock_loop<PRUNE, INCL, EXACT, (EB_MAX_K_DFTSP + 31) / 32>(A);
+}
+template <bool PRUNE, bool INCL, bool EXACT>
+__global__ void __launch_bounds__(EB_WIDE4_THREADS, EB_WIDE4_MINB) dftsp_lock_wide4_kernel(const __grid_constant__ DftspArgs A) {
+  lock_loop<PRUNE, INCL, EXACT, 4>(A);
 }
 
 // Indices of the instances wider than EB_MAX_K (order irrelevant).
@@ -2349,15 +2361,20 @@ static int launch_wide_v2(eb_handle* h, cudaStream_t st, const DftspArgs& A0, in
   W.list_count = buf + 2;
   void (*kern)(DftspArgs);
   const bool P = W.prm.pruning != 0, I = W.prm.inclusive_bound != 0;
-  if (P) {
-    if (I) kern = exact ? dftsp_lock_wide_kernel<true, true, true> : dftsp_lock_wide_kernel<true, true, false>;
-    else kern = exact ? dftsp_lock_wide_kernel<true, false, true> : dftsp_lock_wide_kernel<true, false, false>;
-  } else {
-    if (I) kern = exact ? dftsp_lock_wide_kernel<false, true, true> : dftsp_lock_wide_kernel<false, true, false>;
-    else kern = exact ? dftsp_lock_wide_kernel<false, false, true> : dftsp_lock_wide_kernel<false, false, false>;
+#define EB_PICKW(KN)                                                                                   \
+  if (P) {                                                                                             \
+    if (I) kern = exact ? KN<true, true, true> : KN<true, true, false>;                                \
+    else kern = exact ? KN<true, false, true> : KN<true, false, false>;                                \
+  } else {                                                                                             \
+    if (I) kern = exact ? KN<false, true, true> : KN<false, true, false>;                              \
+    else kern = exact ? KN<false, false, true> : KN<false, false, false>;                              \
   }
+  const bool ni4 = Kw <= 128;
+  if (ni4) { EB_PICKW(dftsp_lock_wide4_kernel) } else { EB_PICKW(dftsp_lock_wide_kernel) }
+#undef EB_PICKW
   int warps = (int)(smem_cap / W.warp_bytes);
-  if (warps > 2) warps = 2;
+  const int wmax = ni4 ? EB_WIDE4_THREADS / 32 : 2;
+  if (warps > wmax) warps = wmax;
   const int64_t n_launch = n_wide > 0 ? n_wide : W.n_inst;        // grid bound only
   int rc = launch_one(h, st, kern, W, warps, W.warp_bytes * warps, n_launch);
   if (rc) return rc;
