@@ -16,6 +16,7 @@
 // feasible rank.  Threads count checked combinations and pruned prefixes into
 // the handle's counters (eb_exhaustive_counters).
 #include <climits>
+#include <cstdlib>
 
 #include "eb_internal.cuh"
 
@@ -545,9 +546,17 @@ int exh_range(eb_handle* h, cudaStream_t st, const eb_context& ctx_host, const e
   const int64_t span = hi - lo;
   const int threads = 256;
   const int64_t max_threads = (int64_t)h->num_sms * 8 * threads;
-  // ~8 chunks per resident thread (dynamic: early finishers take more), >= 64 ranks each
-  int64_t per = span / (max_threads * 8) + 1;
-  if (per < 64) per = 64;
+  // ~2 chunks per resident thread (dynamic: early finishers take more), >= 64
+  // ranks each.  Measured on the K=32 adversarial family (bench.py --config
+  // 4): 8 chunks per thread 86 inst/s, 4: 121, 2: 149, 1: 140 -- smaller
+  // chunks pay an unranking and a global atomic each and scan further past
+  // the answer before the stop flag is seen.  (EB_BRUTE_CHUNKS /
+  // EB_BRUTE_MINCHUNK: tuning)
+  int64_t cpt = 2, minc = 64;
+  if (const char* e = getenv("EB_BRUTE_CHUNKS")) { const long v = atol(e); if (v >= 1 && v <= 1024) cpt = v; }
+  if (const char* e = getenv("EB_BRUTE_MINCHUNK")) { const long v = atol(e); if (v >= 1) minc = v; }
+  int64_t per = span / (max_threads * cpt) + 1;
+  if (per < minc) per = minc;
   A.per = per;
   A.best = d_best; A.status = d_status; A.stats = exh_stats(h);
   const int64_t nchunks = (span + per - 1) / per;

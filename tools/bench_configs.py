@@ -224,24 +224,42 @@ def config3(threads, n_per_k):
 
 
 def config4(ks, per_k):
+    """Brute force (exhaustive_optimal subsets mode) at K = 28..32 on the
+    adversarial family (synth.brute_family) and on config-2-style pools.
+    Rates are instances/s and the device's checked combinations/s
+    (brute.enum_stats); reference-accounted nodes are reported separately and
+    are not an enumeration rate."""
     import torch
     out = []
     for K in ks:
+        fams = [("adversarial", synth.brute_family(K, per_k, seed=2405_0714 + K))]
         w = synth.Workload(f"config4 K={K}", K=K)
         b = synth.generate(w, per_k, seed=2405_0715 + K)
         dres = search.solve_batch(b, ladder=(128, 256, 512))
+        pools = []
         for i in range(per_k):
             lo, hi = int(b.offsets[i]), int(b.offsets[i + 1])
             cols = {k: np.ascontiguousarray(v[lo:hi]) for k, v in b.columns.items()}
-            rec = b.contexts[int(b.ctx_index[i]):int(b.ctx_index[i]) + 1].copy()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            r = brute.solve_sharded(rec, cols, world=1)
-            dt = time.perf_counter() - t0
-            out.append({"K": K, "z": r.z, "dftsp_z": int(dres.z_found[i]), "optimality_ok": r.z == int(dres.z_found[i]),
-                        "nodes_visited": r.nodes_visited, "seconds": round(dt, 4),
-                        "subsets_per_s": round(r.nodes_visited / dt, 1),
-                        "reference_extrapolated_s_1core": round(r.nodes_visited / 6.0e4, 1)})
+            pools.append((b.contexts[int(b.ctx_index[i]):int(b.ctx_index[i]) + 1].copy(), cols))
+        fams.append(("config2-style", pools))
+        for name, insts in fams:
+            for j, (rec, cols) in enumerate(insts):
+                torch.cuda.synchronize()
+                s0 = brute.enum_stats()
+                t0 = time.perf_counter()
+                r = brute.solve_sharded(rec, cols, world=1)
+                torch.cuda.synchronize()
+                dt = time.perf_counter() - t0
+                chk = brute.enum_stats() - s0
+                row = {"K": K, "family": name, "z": r.z, "lexrank": r.lexrank, "seconds": round(dt, 5),
+                       "checked_subsets": int(chk[0]), "pruned_prefixes": int(chk[1]),
+                       "checked_subsets_per_s": round(int(chk[0]) / dt, 1),
+                       "reference_nodes_visited": r.nodes_visited,
+                       "reference_extrapolated_s_1core": round(r.nodes_visited / 6.0e4, 1)}
+                if name == "config2-style":
+                    row["dftsp_z"] = int(dres.z_found[j])
+                    row["optimality_ok"] = r.z == int(dres.z_found[j])
+                out.append(row)
     return {"config": "config4: brute force 2^K (subsets mode), rank-range level search", "rows": out}
 
 
