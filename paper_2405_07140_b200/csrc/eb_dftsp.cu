@@ -1291,15 +1291,15 @@ __device__ __noinline__ void write_status(const eb_dftsp_result& O, int64_t inst
     for (int j = lane; j < n; j += 32) O.solution[r0 + j] = -1;
 }
 
-// FK > 0: the launch's layout is make_lay(FK, EB_FIXED_G, EXACT, v2), known
-// at compile time (shared-memory offsets become immediates); 0: A.lay.
-#define EB_FIXED_G 3
+// FK > 0: the launch's layout is make_lay(FK / 100, FK % 100, EXACT, v2)
+// (K bound, class bound), known at compile time -- shared-memory offsets
+// become immediates; 0: A.lay.
 template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI, int FK = 0>
 __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* smem, int& passed,
                                bool have_meta = false, int64_t m_row0 = 0, int64_t m_row1 = 0, int m_ci = 0) {
   const int lane = threadIdx.x & 31;
   const int K = A.K, G = A.G;
-  constexpr Lay LF = make_lay(FK > 0 ? FK : 1, EB_FIXED_G, EXACT, ALGO == 2);
+  constexpr Lay LF = make_lay(FK > 0 ? FK / 100 : 1, FK > 0 ? FK % 100 : 1, EXACT, ALGO == 2);
   const Lay& L = FK > 0 ? LF : A.lay;       // computed once on the host (make_lay)
   double* a_tau = (double*)(smem + L.a_tau);
   double* a_key = (double*)(smem + L.a_key);
@@ -2112,7 +2112,7 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   __shared__ int s_q[3];           // round bases, two rounds ahead (ring of 3)
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  constexpr size_t WB = al8(make_lay(FK > 0 ? FK : 1, EB_FIXED_G, EXACT, true).total);
+  constexpr size_t WB = al8(make_lay(FK > 0 ? FK / 100 : 1, FK > 0 ? FK % 100 : 1, EXACT, true).total);
   unsigned char* smem = smem_all + warp * (FK > 0 ? WB : A.warp_bytes);
   const int64_t total = A.list_count ? (int64_t)*A.list_count : A.n_inst;
   auto inst_of = [&](int64_t slot) -> int64_t { return A.inst_list ? (int64_t)A.inst_list[slot] : slot; };
@@ -2419,17 +2419,24 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   }
   if (algo != 1 && al8(make_lay(K, G, exact, true).total) * 2 > smem_cap) algo = 1;
   if (algo != 1) algo = 2;
-  // K <= 32 with at most EB_FIXED_G classes (the paper's ladder): the
-  // leaf-parallel kernel with the layout of K = 32 compiled in
-  const bool fixed = algo == 2 && K <= 32 && G <= EB_FIXED_G;
-  A.lay = fixed ? make_lay(32, EB_FIXED_G, exact, true) : make_lay(K, G, exact, algo == 2);
+  // Leaf-parallel kernels with the layout compiled in (FK = 100 K + G):
+  // K <= 32 with the paper's three-class ladder (every flag set), and with
+  // pruning on, K <= 20 with four or five classes (config 5) and K = 33..64
+  // with three classes (config 3's wide end).
+  const bool P = prm.pruning != 0, I = prm.inclusive_bound != 0;
+  int fk = 0;
+  if (algo == 2) {
+    if (K <= 32 && G <= 3) fk = 3203;
+    else if (P && K <= 20 && G <= 5) fk = 2005;
+    else if (P && K <= 64 && G <= 3) fk = 6403;
+  }
+  A.lay = fk ? make_lay(fk / 100, fk % 100, exact, true) : make_lay(K, G, exact, algo == 2);
   A.warp_bytes = al8(A.lay.total);
   int warps = (int)(smem_cap / A.warp_bytes);
   if (warps > 4) warps = 4;
   if (warps < 1) { set_error("instance size K=%d needs %zu B shared memory per warp", K, A.warp_bytes); return EB_ERR_K_TOO_LARGE; }
   size_t smem = A.warp_bytes * warps;
   void (*kern)(DftspArgs);
-  const bool P = prm.pruning != 0, I = prm.inclusive_bound != 0;
 #define EB_PICK3(AL, NI)                                                                           \
   if (P) {                                                                                         \
     if (I) kern = exact ? dftsp_kernel<true, true, true, AL, NI> : dftsp_kernel<true, true, false, AL, NI>;   \
@@ -2457,7 +2464,14 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
     // 8-warp block.  EB_LOCK_WARPS caps the width (tuning).
     int cap_w = 8;
     if (const char* e = getenv("EB_LOCK_WARPS")) { int v = atoi(e); if (v >= 1 && v <= 16) cap_w = v; }
-    if (fixed) { EB_PICKL3(1, 32) } else if (K <= 32) { EB_PICKL3(1, 0) } else { EB_PICKL3(2, 0) }
+#define EB_PICKLP(NI, FK)                                                                              \
+  kern = I ? (exact ? dftsp_lock_kernel<true, true, true, NI, FK> : dftsp_lock_kernel<true, true, false, NI, FK>)    \
+           : (exact ? dftsp_lock_kernel<true, false, true, NI, FK> : dftsp_lock_kernel<true, false, false, NI, FK>);
+    if (fk == 3203) { EB_PICKL3(1, 3203) }
+    else if (fk == 2005) { EB_PICKLP(1, 2005) }
+    else if (fk == 6403) { EB_PICKLP(2, 6403) }
+    else if (K <= 32) { EB_PICKL3(1, 0) } else { EB_PICKL3(2, 0) }
+#undef EB_PICKLP
     {
       struct WCache { void (*k)(DftspArgs); size_t wb; int cap; int dev; int w; };
       static thread_local WCache wc[8];
