@@ -23,7 +23,7 @@ has dftsp    && run ncu_dftsp $NCU -k regex:'dftsp_lock_kernel' -c 1 -o $O/dftsp
                     python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e
 has c5ncu    && run ncu_c5 $NCU -k regex:'dftsp_lock_kernel' -c 1 -o $O/config5 -f \
                     python bench.py --config 5 --steps 1 --warmup 0 --no-cpu --no-e2e
-has wide     && run ncu_wide $NCU -k regex:'dftsp_lock_wide_kernel' -c 1 -o $O/wide -f \
+has wide     && run ncu_wide $NCU -k regex:'dftsp_lock_wide' -c 1 -o $O/wide -f \
                     python tools/run_workload.py --K 120 --n 20000
 has brute    && run ncu_brute $NCU -k regex:'exh_(range|levels|batch)_kernel' -c 6 -o $O/brute -f \
                     python bench.py --config 4 --steps 1 --warmup 0
