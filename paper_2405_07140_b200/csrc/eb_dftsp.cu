@@ -1269,6 +1269,63 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
 
 // Error / empty exit of one instance (kept out of line: one copy serves
 // every early-exit site, which keeps the kernel's instruction footprint small).
+// Per-context constants of the search, derived with the reference's exact
+// operations once per context -- per block for the lockstep kernels' first
+// EB_DC_CACHE contexts, per warp otherwise -- instead of once per instance.
+// The integer polynomials of the padded length are expanded (exact
+// integers): gen_base(s) = gb0 + fd4 s, flops_initial(s) = s (fa + fb s).
+struct DCtx {
+  Ctx c;
+  int64_t m1, kv, gb0, fd4, fa, fb;
+  double headroom, k2, k5, slot_base;
+  double sb_up, sb_dn;                      // T_up * B_up, T_dn * B_dn (radio.py:75, :83)
+  double g_a, g_b, g_c, g_w, g_m;           // overflow-guard polynomials (estimates, 4x margin)
+};
+#define EB_DC_CACHE 8
+
+__device__ __noinline__ void derive_dctx(const eb_context* p, DCtx& D) {
+  const Ctx C = load_ctx(p);
+  D.c = C;
+  const int64_t L = C.m.L, d = C.m.d, f = C.m.ffn;
+  D.m1 = weight_bytes(C.m);                                  // costs.py:62-67
+  D.kv = kv_per_token(C.m);                                  // costs.py:70-72
+  D.gb0 = 8 * d * d + 4 * d * f;                             // feasibility.py:155 without the s term
+  D.fd4 = 4 * d;
+  D.fa = L * (8 * d * d + 4 * d * f);                        // costs.py:87-97 expanded in s
+  D.fb = 4 * L * d;
+  D.headroom = sub(div(C.M, C.alpha), i2d(D.m1));            // feasibility.py:144
+  D.k2 = div(D.headroom, i2d(D.kv));                         // feasibility.py:152
+  D.k5 = i2d(2 * L * d);                                     // feasibility.py:159
+  D.slot_base = C.has_cap ? div(mul(C.cap_s, C.C), C.beta) : 0.0;   // feasibility.py:124
+  D.sb_up = mul(C.T_up, C.B_up);
+  D.sb_dn = mul(C.T_dn, C.B_dn);
+  const double Ld = (double)L, dd = (double)d, fd = (double)f, bp = (double)C.m.bpp;
+  D.g_a = Ld * (8.0 * dd * dd + 4.0 * dd * fd);
+  D.g_b = Ld * 4.0 * dd;
+  D.g_c = Ld * 2.0 * dd;
+  D.g_w = Ld * (4.0 * bp * dd * (double)C.m.head_dim * (double)C.m.heads + 2.0 * bp * dd * fd);
+  D.g_m = 2.0 * bp * Ld * dd;
+}
+
+// uplink / downlink fractions per token (radio.py:71-84) with the slot x
+// band products of the context precomputed (same operations, same order)
+__device__ __forceinline__ int k_up_d(const DCtx& D, double gain, double pup, double* out) {
+  const Ctx& c = D.c;
+  if (pup <= 0.0 || gain <= 0.0 || c.N0_up <= 0.0) { *out = 0.0; return EB_ERR_NONPOSITIVE_LINK; }
+  const double eff = spectral_efficiency(pup, gain, c.N0_up);
+  if (eff <= 0.0) { *out = 0.0; return EB_ERR_UPLINK_EFF_ZERO; }    // radio.py:74
+  *out = div(c.fbits, mul(D.sb_up, eff));
+  return 0;
+}
+__device__ __forceinline__ int k_dn_d(const DCtx& D, double gain, double* out) {
+  const Ctx& c = D.c;
+  if (c.P_dn <= 0.0 || gain <= 0.0 || c.N0_dn <= 0.0) { *out = 0.0; return EB_ERR_NONPOSITIVE_LINK; }
+  const double eff = spectral_efficiency(c.P_dn, gain, c.N0_dn);
+  if (eff <= 0.0) { *out = 0.0; return EB_ERR_DOWNLINK_EFF_ZERO; }  // radio.py:82
+  *out = div(c.fbits, mul(D.sb_dn, eff));
+  return 0;
+}
+
 __device__ __noinline__ void write_status(const eb_dftsp_result& O, int64_t inst, int64_t r0, int n, int st,
                                           int err) {
   const int lane = threadIdx.x & 31;
@@ -1296,6 +1353,7 @@ __device__ __noinline__ void write_status(const eb_dftsp_result& O, int64_t inst
 // become immediates; 0: A.lay.
 template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI, int FK = 0>
 __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* smem, int& passed,
+                               const DCtx* dcache, int ncache, DCtx* dslot,
                                bool have_meta = false, int64_t m_row0 = 0, int64_t m_row1 = 0, int m_ci = 0) {
   const int lane = threadIdx.x & 31;
   const int K = A.K, G = A.G;
@@ -1346,7 +1404,13 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   if (ci < 0 || ci >= A.n_ctx) { put_status(EB_ERR_INVALID_ARG, -1); return; }
   if (n == 0) { put_status(EB_OK, -1); return; }     // dftsp.py:253-254
   if (n > K || n > 32 * NI) { put_status(EB_ERR_K_TOO_LARGE, -1); return; }
-  const Ctx C = load_ctx(&A.ctxs[ci]);
+  const DCtx* D = dcache + ci;
+  if (ci >= ncache) {
+    if (lane == 0) derive_dctx(&A.ctxs[ci], *dslot);
+    __syncwarp();
+    D = dslot;
+  }
+  const Ctx& C = D->c;
 
   // ---------------- setup: per request (lanes over i = lane, lane+32) -----
   int s_i[NI], len_i[NI];
@@ -1438,27 +1502,24 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     for (int h = 0; h < NI; ++h)
       if (lane + 32 * h < n) nmx = max(nmx, len_i[h]);
     nmx = __reduce_max_sync(EB_FULL, nmx);
-    const double Ld = (double)C.m.L, dd = (double)C.m.d, fd = (double)C.m.ffn, s = (double)padded, o = (double)nmx;
-    const double bp = (double)C.m.bpp;
-    const double fi = Ld * (8.0 * s * dd * dd + 4.0 * s * s * dd + 4.0 * s * dd * fd);
-    const double far = Ld * o * (8.0 * dd * dd + 4.0 * s * dd + 4.0 * dd * fd + 2.0 * dd * o);
-    const double w = Ld * (4.0 * bp * dd * (double)C.m.head_dim * (double)C.m.heads + 2.0 * bp * dd * fd);
-    const double mem = w + 2.0 * bp * Ld * dd * (s + o) * (double)n;
+    const double s = (double)padded, o = (double)nmx;
+    const double fi = s * (D->g_a + D->g_b * s);              // flops_initial(s)
+    const double far = o * (D->g_a + D->g_b * s + D->g_c * o); // flops_autoregressive(s, o)
+    const double mem = D->g_w + D->g_m * (s + o) * (double)n;
     if ((double)n * (fi + far) > 0x1p61 || mem > 0x1p61) { put_status(EB_ERR_OVERFLOW, -1); return; }
   }
 
   // derive_coefficients feasibility.py:133-167
-  const int64_t m1 = weight_bytes(C.m);
-  const double headroom = sub(div(C.M, C.alpha), i2d(m1));
-  if (headroom < 0) { put_status(EB_ERR_WEIGHTS_DO_NOT_FIT, -1); return; }
-  const int64_t kv = kv_per_token(C.m);
-  const int64_t gb = gen_base(C.m, padded);
-  const int64_t fi_pad = flops_initial(C.m, padded);
-  const double k2 = div(headroom, i2d(kv));
+  const int64_t m1 = D->m1;
+  if (D->headroom < 0) { put_status(EB_ERR_WEIGHTS_DO_NOT_FIT, -1); return; }
+  const int64_t kv = D->kv;
+  const int64_t gb = D->gb0 + D->fd4 * padded;                        // gen_base(padded)
+  const int64_t fi_pad = (int64_t)padded * (D->fa + D->fb * padded);  // flops_initial(padded)
+  const double k2 = D->k2;
   const double k3 = i2d(fi_pad - C.m.L * gb);
   const double k4 = i2d(C.m.L * (gb - 2 * C.m.d));
-  const double k5 = i2d(2 * C.m.L * C.m.d);
-  const double slot_base = C.has_cap ? div(mul(C.cap_s, C.C), C.beta) : 0.0;  // feasibility.py:124
+  const double k5 = D->k5;
+  const double slot_base = D->slot_base;                              // feasibility.py:124
 
   double key_i[NI], dnt_i[NI], tau_i[NI];
   int err_link = INT_MAX, err_code = 0;
@@ -1468,8 +1529,8 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     key_i[h] = dnt_i[h] = tau_i[h] = 0.0;
     if (i < n) {
       double ku, kd;
-      int st = k_up_of(C, g_i[h], p_i[h], &ku);
-      if (!st) st = k_dn_of(C, g_i[h], &kd);
+      int st = k_up_d(*D, g_i[h], p_i[h], &ku);
+      if (!st) st = k_dn_d(*D, g_i[h], &kd);
       if (st) {
         if (i < err_link) { err_link = i; err_code = st; }
       } else {
@@ -1980,7 +2041,8 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       // batch_cost at the batch's own padding (sim.py:372-376)
       pb = __reduce_max_sync(EB_FULL, pb);
       const int64_t mem_b = m1 + kv * (int64_t)pb * zf + kv * sn;
-      const int64_t fl_batch = (int64_t)zf * flops_initial(C.m, pb) + C.m.L * (gen_base(C.m, pb) * s1 + 2 * C.m.d * s2);
+      const int64_t fl_batch = (int64_t)zf * ((int64_t)pb * (D->fa + D->fb * pb)) +
+                               C.m.L * ((D->gb0 + D->fd4 * pb) * s1 + 2 * C.m.d * s2);
       met[EB_MET_UP_SUM] = up;
       met[EB_MET_DN_SUM] = dn;
       met[EB_MET_MEM_POOLPAD] = mul(C.alpha, i2d(mem));
@@ -2058,6 +2120,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
 template <bool PRUNE, bool INCL, bool EXACT, int ALGO, int NI>
 __global__ void __launch_bounds__(128, 4) dftsp_kernel(const __grid_constant__ DftspArgs A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
+  __shared__ DCtx s_dw[4];
   const int warp = threadIdx.x >> 5;
   unsigned char* smem = smem_all + warp * A.warp_bytes;
   // second (fallback) pass: only instances v2 flagged, and nothing at all
@@ -2070,7 +2133,7 @@ __global__ void __launch_bounds__(128, 4) dftsp_kernel(const __grid_constant__ D
     if (inst >= A.n_inst) break;
     if (A.fallback_pass && A.out.status[inst] != EB_STATUS_FALLBACK) continue;
     int passed = 0;
-    solve_instance<PRUNE, INCL, EXACT, ALGO, NI>(A, inst, smem, passed);
+    solve_instance<PRUNE, INCL, EXACT, ALGO, NI>(A, inst, smem, passed, nullptr, 0, &s_dw[warp]);
     __syncwarp();
   }
 }
@@ -2084,6 +2147,7 @@ __global__ void __launch_bounds__(128, 4) dftsp_kernel(const __grid_constant__ D
 template <bool PRUNE, bool INCL, bool EXACT>
 __global__ void __launch_bounds__(32, 1) dftsp_wide_kernel(const __grid_constant__ DftspArgs A, unsigned char* gscratch) {
   extern __shared__ __align__(16) unsigned char smem_all[];
+  __shared__ DCtx s_dw;
   unsigned char* smem = gscratch ? gscratch + (size_t)blockIdx.x * A.warp_bytes : smem_all;
   for (;;) {
     int64_t inst = 0;
@@ -2094,7 +2158,7 @@ __global__ void __launch_bounds__(32, 1) dftsp_wide_kernel(const __grid_constant
     if (n <= EB_MAX_K || n > EB_MAX_K_DFTSP) continue;
     if (A.fallback_pass && A.out.status[inst] != EB_STATUS_FALLBACK) continue;   // after the v2 wide pass
     int passed = 0;
-    solve_instance<PRUNE, INCL, EXACT, 1, (EB_MAX_K_DFTSP + 31) / 32>(A, inst, smem, passed);
+    solve_instance<PRUNE, INCL, EXACT, 1, (EB_MAX_K_DFTSP + 31) / 32>(A, inst, smem, passed, nullptr, 0, &s_dw);
     __syncwarp();
   }
 }
@@ -2111,6 +2175,8 @@ template <bool PRUNE, bool INCL, bool EXACT, int NI, int FK = 0>
 __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   __shared__ int s_q[3];           // round bases, two rounds ahead (ring of 3)
+  __shared__ DCtx s_dc[EB_DC_CACHE];   // derived constants of the first contexts
+  __shared__ DCtx s_dw[16];            // per warp: a context past the cache
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   constexpr size_t WB = al8(make_lay(FK > 0 ? FK / 100 : 1, FK > 0 ? FK % 100 : 1, EXACT, true).total);
   unsigned char* smem = smem_all + warp * (FK > 0 ? WB : A.warp_bytes);
@@ -2128,6 +2194,8 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
     }
   };
   if (threadIdx.x == 0) { s_q[0] = atomicAdd(A.counter, nw); s_q[1] = atomicAdd(A.counter, nw); }
+  const int ncache = A.n_ctx < EB_DC_CACHE ? A.n_ctx : EB_DC_CACHE;
+  if (threadIdx.x < ncache) derive_dctx(&A.ctxs[threadIdx.x], s_dc[threadIdx.x]);
   __syncthreads();
   int64_t base = s_q[0], nxt = s_q[1];
   int64_t c0 = 0, c1 = 0, a0 = 0, a1 = 0;
@@ -2139,7 +2207,9 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
     meta_of(nxt + warp, a0, a1, aci);
     const int64_t slot = base + warp;
     int passed = 0;
-    if (slot < total) solve_instance<PRUNE, INCL, EXACT, 2, NI, FK>(A, inst_of(slot), smem, passed, true, c0, c1, cci);
+    if (slot < total)
+      solve_instance<PRUNE, INCL, EXACT, 2, NI, FK>(A, inst_of(slot), smem, passed, s_dc, ncache, &s_dw[warp], true, c0,
+                                                   c1, cci);
     __syncwarp();
     for (; passed < 3; ++passed)
       if ((EB_LOCK_BARRIERS >> passed) & 1) __syncthreads();
