@@ -113,7 +113,7 @@ __host__ __device__ constexpr inline Lay make_lay(int K, int G, bool exact, bool
   } else {
     L.pq = L.pre = L.pf = L.pm = 0;
   }
-  L.total = o;
+  L.total = (o + 15) & ~size_t(15);   // 16-byte warp stride: a_tau (offset 0) is read as double2
   return L;
 }
 
@@ -138,6 +138,17 @@ struct DftspArgs {
   int fallback_pass;
 };
 
+// sum of the 8-bit counts of levels [0, k) (every count <= 64 and their
+// total <= 64, so the byte-sum multiply never carries between bytes)
+__device__ __forceinline__ int sumV_below(uint64_t v0, uint64_t v1, int k) {
+  const uint64_t m0 = k >= 8 ? ~0ULL : ((1ULL << (8 * k)) - 1ULL);
+  int s = (int)(((v0 & m0) * 0x0101010101010101ULL) >> 56);
+  if (k > 8) {
+    const uint64_t m1 = k >= 16 ? ~0ULL : ((1ULL << (8 * (k - 8))) - 1ULL);
+    s += (int)(((v1 & m1) * 0x0101010101010101ULL) >> 56);
+  }
+  return s;
+}
 __device__ __forceinline__ int getV(uint64_t v0, uint64_t v1, int k) {
   return (int)(((k < 8) ? (v0 >> (8 * k)) : (v1 >> (8 * (k - 8)))) & 0xff);
 }
@@ -1587,8 +1598,14 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
         // tau rank: requests with a larger tau, then equal-tau requests with a
         // smaller id (lanes holding the same tau, by a match; -0.0 is
         // folded onto +0.0 so that equal doubles match)
-#pragma unroll 4
-        for (int j = 0; j < n; ++j) t += (int)(a_tau[j] > tau_i[h]);
+        const double2* a_tau2 = (const double2*)a_tau;
+        int j = 0;
+#pragma unroll 2
+        for (; j + 1 < n; j += 2) {
+          const double2 v = a_tau2[j >> 1];
+          t += (int)(v.x > tau_i[h]) + (int)(v.y > tau_i[h]);
+        }
+        if (j < n) t += (int)(a_tau[j] > tau_i[h]);
         first = (peers & lanemask_lt()) == 0;
       } else {
         // one branch-free pass: tau rank, class leadership, within-class rank
@@ -1686,18 +1703,18 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       }
     }
   }
-  if (lane < Gi) c_cnt[lane] = 0;
-  __syncwarp();
+  {
+    // class sizes and starts: one ballot per class and 32-request slice
+    int acc = 0, my_start = 0, my_cnt = 0;
+    for (int g = 0; g < Gi; ++g) {
+      int cg = 0;
 #pragma unroll
-  for (int h = 0; h < NI; ++h) {
-    int i = lane + 32 * h;
-    if (i < n) atomicAdd(&c_cnt[gcls_i[h]], 1);
-  }
-  __syncwarp();
-  if (lane == 0) {
-    int acc = 0;
-    for (int g = 0; g < Gi; ++g) { c_start[g] = acc; acc += c_cnt[g]; }
-    c_start[Gi] = acc;
+      for (int h = 0; h < NI; ++h) cg += __popc(__ballot_sync(EB_FULL, lane + 32 * h < n && gcls_i[h] == g));
+      if (lane == g) { my_start = acc; my_cnt = cg; }
+      acc += cg;
+    }
+    if (lane < Gi) { c_start[lane] = my_start; c_cnt[lane] = my_cnt; }
+    if (lane == 0) c_start[Gi] = acc;
   }
   __syncwarp();
 #pragma unroll
@@ -1931,9 +1948,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
         const int kk = __popc(present & ((1u << g) - 1u));
         const int cnt = (kk <= kwin) ? getV(W0, W1, kk) : 0;
         if (rk < cnt) {
-          int base = 0;
-          for (int k2 = 0; k2 < kk && k2 <= kwin; ++k2) base += getV(W0, W1, k2);
-          sol[base + rk] = (uint8_t)t;
+          sol[sumV_below(W0, W1, kk) + rk] = (uint8_t)t;     // kk <= kwin here (cnt > 0)
         }
       }
     } else if constexpr (NI == 2) {
@@ -1966,9 +1981,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
         const int kk = __popc(present & ((1u << g) - 1u));
         const int cnt = (kk <= kwin) ? getV(W0, W1, kk) : 0;
         if (rk < cnt) {
-          int base = 0;
-          for (int k2 = 0; k2 < kk && k2 <= kwin; ++k2) base += getV(W0, W1, k2);
-          sol[base + rk] = (uint8_t)tt[h];
+          sol[sumV_below(W0, W1, kk) + rk] = (uint8_t)tt[h];   // kk <= kwin here (cnt > 0)
         }
       }
     } else if (lane == 0) {
