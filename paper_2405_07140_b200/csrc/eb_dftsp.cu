@@ -1202,6 +1202,40 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
   for (int d = dwin; found && d == dwin; ++d) {
     const int m = ncls_d[d - 1];
     const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
+    if (ctab != nullptr && m <= 3 && d <= EB_MAX_K && !traj) {
+      // Tabulated shape: the calls r > zf of the winning width are one
+      // difference of the partition's row (as for the other widths), and the
+      // winner's partial count reads PF_{j+1} -- the prefix sums of the level
+      // below j -- from the row of the suffix partition (levels j+1 .. m-1):
+      // F(j+1, .) depends only on the suffix's sizes and tails, which is what
+      // that row tabulates.  The indices stay below the suffix's total (the
+      // path reaches the winning leaf), inside the row.
+      if (lane == 0) {
+        const uint2* CT0 = (const uint2*)((const unsigned char*)ctab + CT_HDR_BYTES);
+        const uint2* T = CT0 + (size_t)ct_row_closed(m, row[0].size, m > 1 ? row[1].size : 0,
+                                                     m > 2 ? row[2].size : 0) * CT;
+        my_v += (uint64_t)(T[d].x - T[zf].x) + (uint64_t)(d - zf);      // + one root per call
+        my_p += (uint64_t)(T[d].y - T[zf].y);
+        uint64_t fv = 1, fp = 0;
+        int rr = zf;
+        for (int j = 0; j < kwin; ++j) {
+          const int c = getV(W0, W1, j);
+          const int x0 = min(rr, (int)row[j].size);
+          const int xb = (x0 == rr) ? x0 - 1 : x0;
+          fv += (uint64_t)(x0 - c) + 1;
+          if (xb >= c + 1) {
+            const int ms = m - j - 1;                                    // suffix levels (>= 1)
+            const uint2* S = CT0 + (size_t)ct_row_closed(ms, row[j + 1].size, ms > 1 ? row[j + 2].size : 0, 0) * CT;
+            fv += (uint64_t)(S[rr - c - 1].x - S[rr - xb - 1].x);
+            fp += (uint64_t)(S[rr - c - 1].y - S[rr - xb - 1].y);
+          }
+          rr -= c;
+        }
+        my_v += fv + 1;                                                  // the leaf itself
+        my_p += fp;
+      }
+      continue;
+    }
     const int kc = m - 1;    // all levels (the partial count walks them)
     for (int k = kc; k >= 1; --k) {
       const uint64_t* NV = pfv + (size_t)(k + 1) * (n + 1);
