@@ -1202,7 +1202,9 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
   for (int d = dwin; found && d == dwin; ++d) {
     const int m = ncls_d[d - 1];
     const LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
-    if (ctab != nullptr && m <= 3 && d <= EB_MAX_K && !traj) {
+    const uint2* ctab_m = (ctab != nullptr && (m == 4 || m == 5) && d <= CTM_K && !traj)
+                              ? *(const uint2* const*)((const unsigned char*)ctab + CT_MPTR_OFF) : nullptr;
+    if (ctab != nullptr && !traj && ((m <= 3 && d <= EB_MAX_K) || ctab_m != nullptr)) {
       // Tabulated shape: the calls r > zf of the winning width are one
       // difference of the partition's row (as for the other widths), and the
       // winner's partial count reads PF_{j+1} -- the prefix sums of the level
@@ -1212,8 +1214,15 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
       // path reaches the winning leaf), inside the row.
       if (lane == 0) {
         const uint2* CT0 = (const uint2*)((const unsigned char*)ctab + CT_HDR_BYTES);
-        const uint2* T = CT0 + (size_t)ct_row_closed(m, row[0].size, m > 1 ? row[1].size : 0,
-                                                     m > 2 ? row[2].size : 0) * CT;
+        auto trow = [&](int j0, int ms) -> const uint2* {     // levels j0 .. j0 + ms - 1
+          if (ms <= 3)
+            return CT0 + (size_t)ct_row_closed(ms, row[j0].size, ms > 1 ? row[j0 + 1].size : 0,
+                                               ms > 2 ? row[j0 + 2].size : 0) * CT;
+          int t = 0, rank = ms == 5 ? CTM_ROWS4 : 0;         // ctm_row over the sizes
+          for (int i = 0; i < ms; ++i) { t += row[j0 + i].size; rank += binom_small(t - 1, i + 1); }
+          return ctab_m + (size_t)rank * CTM;
+        };
+        const uint2* T = trow(0, m);
         my_v += (uint64_t)(T[d].x - T[zf].x) + (uint64_t)(d - zf);      // + one root per call
         my_p += (uint64_t)(T[d].y - T[zf].y);
         uint64_t fv = 1, fp = 0;
@@ -1224,8 +1233,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
           const int xb = (x0 == rr) ? x0 - 1 : x0;
           fv += (uint64_t)(x0 - c) + 1;
           if (xb >= c + 1) {
-            const int ms = m - j - 1;                                    // suffix levels (>= 1)
-            const uint2* S = CT0 + (size_t)ct_row_closed(ms, row[j + 1].size, ms > 1 ? row[j + 2].size : 0, 0) * CT;
+            const uint2* S = trow(j + 1, m - j - 1);                     // suffix levels (>= 1)
             fv += (uint64_t)(S[rr - c - 1].x - S[rr - xb - 1].x);
             fp += (uint64_t)(S[rr - c - 1].y - S[rr - xb - 1].y);
           }
