@@ -149,11 +149,16 @@ __device__ __forceinline__ int sumV_below(uint64_t v0, uint64_t v1, int k) {
   }
   return s;
 }
+// V8: at most 8 levels known at compile time (the compiled-in layouts), so
+// every count sits in v0
+template <bool V8 = false>
 __device__ __forceinline__ int getV(uint64_t v0, uint64_t v1, int k) {
+  if (V8) return (int)((v0 >> (8 * k)) & 0xff);
   return (int)(((k < 8) ? (v0 >> (8 * k)) : (v1 >> (8 * (k - 8)))) & 0xff);
 }
+template <bool V8 = false>
 __device__ __forceinline__ void setV(uint64_t& v0, uint64_t& v1, int k, int x) {
-  if (k < 8) v0 = (v0 & ~(0xffULL << (8 * k))) | ((uint64_t)x << (8 * k));
+  if (V8 || k < 8) v0 = (v0 & ~(0xffULL << (8 * k))) | ((uint64_t)x << (8 * k));
   else v1 = (v1 & ~(0xffULL << (8 * (k - 8)))) | ((uint64_t)x << (8 * (k - 8)));
 }
 
@@ -679,7 +684,7 @@ __device__ __forceinline__ uint32_t pq_closed(const LevelInfo* row, int m, int k
   return (uint32_t)((b + 1) * (s2 + 1) + (a - b) * (x + 1) - (a * (a + 1) - b * (b + 1)) / 2);
 }
 
-template <bool PRUNE, bool INCL, bool EXACT, int NI>
+template <bool PRUNE, bool INCL, bool EXACT, int NI, int FK = 0>
 __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const Lay& L, const LevelInfo* lvl,
                           const uint8_t* ncls_d,
                           const int32_t* c_len, const double* c_w, const double* o_tau, double k2, double k3,
@@ -687,6 +692,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
                           int& dwin, int& kwin, uint64_t& W0, uint64_t& W1, int& best, uint64_t& tot_v,
                           uint64_t& tot_p, const CountsMode& cm, const uint2* ctab, const uint8_t* sizes) {
   const int lane = threadIdx.x & 31;
+  constexpr bool V8 = FK > 0 && FK % 100 <= 8;   // count vectors fit one u64
   uint64_t cm_before = 0;   // counts mode: count vectors tried in completed windows
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
   uint32_t* pq = (uint32_t*)(smem + L.pq);
@@ -964,7 +970,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
             i -= Pv(xa) - pb;
             cc = r - xa;
           }
-          if (cc) { setV(V0, V1, k, cc); klast = k; }
+          if (cc) { setV<V8>(V0, V1, k, cc); klast = k; }
           // SearchTables.build's up[k][cc] / dn[k][cc] / tau_min_prefix[k][cc]
           // (dftsp.py:119-128): the same sequential folds over the class's
           // first cc members among the dd first by tau, in key order
@@ -1009,7 +1015,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
           int64_t mem2 = 0;
           for (int k = 0; k < m; ++k) {
             const LevelInfo li = row[k];
-            const int want = getV(V0, V1, k);
+            const int want = getV<V8>(V0, V1, k);
             if constexpr (NI <= 2) {
               WMask bits = (WMask)pm[dd - 1] & ((WMask)~(WMask)0 << cm.c_start[li.g]);
               for (int q = 0; q < want; ++q) {
@@ -1228,7 +1234,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
         uint64_t fv = 1, fp = 0;
         int rr = zf;
         for (int j = 0; j < kwin; ++j) {
-          const int c = getV(W0, W1, j);
+          const int c = getV<V8>(W0, W1, j);
           const int x0 = min(rr, (int)row[j].size);
           const int xb = (x0 == rr) ? x0 - 1 : x0;
           fv += (uint64_t)(x0 - c) + 1;
@@ -1287,7 +1293,7 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
         int rr = r;
         for (int j = 0; j < kwin; ++j) {
           const LevelInfo lj = row[j];
-          const int c = getV(W0, W1, j);
+          const int c = getV<V8>(W0, W1, j);
           const int x0 = min(rr, (int)lj.size);
           const int xb = (x0 == rr) ? x0 - 1 : x0;
           fv += (uint64_t)(x0 - c) + 1;
@@ -1409,6 +1415,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
                                const DCtx* dcache, int ncache, DCtx* dslot,
                                bool have_meta = false, int64_t m_row0 = 0, int64_t m_row1 = 0, int m_ci = 0) {
   const int lane = threadIdx.x & 31;
+  constexpr bool V8 = FK > 0 && FK % 100 <= 8;   // count vectors fit one u64
   const int K = A.K, G = A.G;
   constexpr Lay LF = make_lay(FK > 0 ? FK / 100 : 1, FK > 0 ? FK % 100 : 1, EXACT, ALGO == 2);
   const Lay& L = FK > 0 ? LF : A.lay;       // computed once on the host (make_lay)
@@ -1868,7 +1875,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   int zf = 0, dwin = 0, kwin = 0;
   uint64_t W0 = 0, W1 = 0;
   if constexpr (ALGO == 2) {
-    if (!search_v2<PRUNE, INCL, EXACT, NI>(passed, n, Gi, smem, L, lvl, ncls_d, c_len, c_w, o_tau, k2, k3,
+    if (!search_v2<PRUNE, INCL, EXACT, NI, FK>(passed, n, Gi, smem, L, lvl, ncls_d, c_len, c_w, o_tau, k2, k3,
                                        slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
                                        tot_v, tot_p,
                                        CountsMode{A.prm.exhaustive_counts != 0, c_start, c_list, o_key, o_dnt},
@@ -1988,7 +1995,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
         const int cs = c_start[g];
         const int rk = __popc(inm & ((1u << lane) - 1u) & ~((1u << cs) - 1u));
         const int kk = __popc(present & ((1u << g) - 1u));
-        const int cnt = (kk <= kwin) ? getV(W0, W1, kk) : 0;
+        const int cnt = (kk <= kwin) ? getV<V8>(W0, W1, kk) : 0;
         if (rk < cnt) {
           sol[sumV_below(W0, W1, kk) + rk] = (uint8_t)t;     // kk <= kwin here (cnt > 0)
         }
@@ -2021,7 +2028,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
           }
         }
         const int kk = __popc(present & ((1u << g) - 1u));
-        const int cnt = (kk <= kwin) ? getV(W0, W1, kk) : 0;
+        const int cnt = (kk <= kwin) ? getV<V8>(W0, W1, kk) : 0;
         if (rk < cnt) {
           sol[sumV_below(W0, W1, kk) + rk] = (uint8_t)tt[h];   // kk <= kwin here (cnt > 0)
         }
@@ -2029,7 +2036,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     } else if (lane == 0) {
       int q = 0;
       for (int kk = 0; kk < wncls; ++kk) {
-        int cnt = (kk <= kwin) ? getV(W0, W1, kk) : 0;
+        int cnt = (kk <= kwin) ? getV<V8>(W0, W1, kk) : 0;
         int g = wrow[kk].g;
         int taken = 0;
         for (int p = c_start[g]; p < c_start[g + 1] && taken < cnt; ++p) {
@@ -2164,7 +2171,7 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     bool live = found && status == EB_OK && lane < wncls;
     int cnt = 0, clen = 0;
     if (live) {
-      cnt = (lane <= kwin) ? getV(W0, W1, lane) : 0;
+      cnt = (lane <= kwin) ? getV<V8>(W0, W1, lane) : 0;
       clen = c_len[wrow[lane].g];
     }
     if (O.counts) O.counts[inst * EB_MAX_CLASSES + lane] = cnt;
