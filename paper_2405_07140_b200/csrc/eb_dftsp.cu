@@ -956,10 +956,28 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
           int cc;
           if (k == m - 1) {
             cc = r;
+          } else if (k + 1 == m - 1) {
+            // one level below: exactly one vector per remaining sum, so the
+            // i-th leaf takes hi - i here (the closed-form search's answer)
+            cc = min(r, (int)li.size) - (int)i;
+            i = 0;
+          } else if (k + 1 == m - 2) {
+            // two levels below: e(x) = #pairs (c1, c2) <= (s1, s2) summing to
+            // x; scan x from the largest count down (the leaf sits in the
+            // first few groups), the same answer as the prefix search
+            const int s1 = row[k + 1].size, s2 = row[k + 2].size;
+            int x = r - min(r, (int)li.size);
+            for (;;) {
+              const uint32_t e = (uint32_t)(min(x, s1) - max(0, x - s2) + 1);
+              if (e > i) break;
+              i -= e;
+              ++x;
+            }
+            cc = r - x;
           } else {                                                 // unrank level k
             const uint32_t* P = base + (size_t)k * W;              // level k+1 prefix
-            // closed form for the last two levels (every level when m <= 3)
-            auto Pv = [&](int y) -> uint32_t { return k >= m - 3 ? pq_closed(row, m, k, y) : P[y]; };
+            // levels with three or more below: the unranking tables
+            auto Pv = [&](int y) -> uint32_t { return P[y]; };
             const int hi = min(r, (int)li.size), lo = max(0, r - (int)li.tail_next);
             const uint32_t pb = Pv(r - hi);
             int xa = r - hi, xz = r - lo;
