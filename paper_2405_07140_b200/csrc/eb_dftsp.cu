@@ -1822,55 +1822,96 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
   // ---------------- per pool width d: class sizes, levels, tables --------
   const int nDG = n * Gi;
   (void)nDG;
-  {
-    // sizes[d][g] = members of class g among the d first in tau order: one
-    // ballot per class and 32-rank slice over lanes = tau ranks, then lanes =
-    // d count the bits below d (earlier slices whole)
+  if constexpr (NI == 1 && FK > 0) {
+    // Compiled-in class bound (FG): lane = tau rank t = width d - 1 computes
+    // its width's class sizes by one ballot per class and builds that width's
+    // level row from registers (the general path below stores the sizes and
+    // reads them back on the same lane).
+    constexpr int FG = FK % 100;
+    const int t = lane, d = lane + 1;
+    const int gt = t < n ? o_g[t] : -1;
+    const unsigned below = (2u << lane) - 1u;
+    int szr[FG];
 #pragma unroll
-    for (int h = 0; h < NI; ++h) {
-      const int t = lane + 32 * h;                            // tau rank; width d = t + 1
-      const int gt = t < n ? o_g[t] : -1;
-      const unsigned below = (t < n) ? ((2u << lane) - 1u) : 0u;
-      for (int g = 0; g < Gi; ++g) {
-        int full = 0;                                         // class g in slices before h
+    for (int g = 0; g < FG; ++g) szr[g] = __popc(__ballot_sync(EB_FULL, gt == g) & below);
+    if (t < n) {
+      const int base = (d - 1) * d / 2 + (d - 1) * Gi;
+      LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
+      int k = 0, start = 0, kn = 0;
 #pragma unroll
-        for (int q = 0; q < h; ++q) {
-          const int tq = lane + 32 * q;
-          full += __popc(__ballot_sync(EB_FULL, tq < n && o_g[tq] == g));
+      for (int g = 0; g < FG; ++g) {
+        if (g < Gi) {
+          const int sz = szr[g];
+          sizes[t * Gi + g] = (uint8_t)sz;
+          if (g == gt) kn = k;        // level of the class the d-th request joined
+          if (sz > 0) {
+            LevelInfo li;
+            li.off = (uint16_t)(base + start);
+            li.size = (uint8_t)sz;
+            li.tail_next = 0;
+            li.g = (uint8_t)g;
+            li.pad[0] = li.pad[1] = li.pad[2] = 0;
+            row[k++] = li;
+          }
+          start += sz + 1;
         }
-        const unsigned mg = __ballot_sync(EB_FULL, gt == g);
-        if (t < n) sizes[t * Gi + g] = (uint8_t)(full + __popc(mg & below));
+      }
+      ncls_d[d - 1] = (uint8_t)k;
+      int tail = 0;
+      for (int q = k - 1; q >= 0; --q) { row[q].tail_next = (uint8_t)tail; tail += row[q].size; }
+      row[0].pad[0] = (uint8_t)kn;
+    }
+  } else {
+  {
+      // sizes[d][g] = members of class g among the d first in tau order: one
+      // ballot per class and 32-rank slice over lanes = tau ranks, then lanes =
+      // d count the bits below d (earlier slices whole)
+  #pragma unroll
+      for (int h = 0; h < NI; ++h) {
+        const int t = lane + 32 * h;                            // tau rank; width d = t + 1
+        const int gt = t < n ? o_g[t] : -1;
+        const unsigned below = (t < n) ? ((2u << lane) - 1u) : 0u;
+        for (int g = 0; g < Gi; ++g) {
+          int full = 0;                                         // class g in slices before h
+  #pragma unroll
+          for (int q = 0; q < h; ++q) {
+            const int tq = lane + 32 * q;
+            full += __popc(__ballot_sync(EB_FULL, tq < n && o_g[tq] == g));
+          }
+          const unsigned mg = __ballot_sync(EB_FULL, gt == g);
+          if (t < n) sizes[t * Gi + g] = (uint8_t)(full + __popc(mg & below));
+        }
       }
     }
-  }
-  __syncwarp();
-  for (int d = lane + 1; d <= n; d += 32) {
-    int base = (d - 1) * d / 2 + (d - 1) * Gi;
-    int k = 0, start = 0;
-    LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
-    // level of the class the d-th request (tau order) joined: the count
-    // recurrence of width d differs from width d-1 only at that level and
-    // above (row[0].pad[0]; meaningful when the class count is unchanged)
-    const int gn = o_g[d - 1];
-    int kn = 0;
-    for (int g = 0; g < Gi; ++g) {
-      int sz = sizes[(d - 1) * Gi + g];
-      if (g == gn) kn = k;
-      if (sz > 0) {
-        LevelInfo li;
-        li.off = (uint16_t)(base + start);
-        li.size = (uint8_t)sz;
-        li.tail_next = 0;
-        li.g = (uint8_t)g;
-        li.pad[0] = li.pad[1] = li.pad[2] = 0;
-        row[k++] = li;
+    __syncwarp();
+    for (int d = lane + 1; d <= n; d += 32) {
+      int base = (d - 1) * d / 2 + (d - 1) * Gi;
+      int k = 0, start = 0;
+      LevelInfo* row = lvl + (size_t)(d - 1) * Gi;
+      // level of the class the d-th request (tau order) joined: the count
+      // recurrence of width d differs from width d-1 only at that level and
+      // above (row[0].pad[0]; meaningful when the class count is unchanged)
+      const int gn = o_g[d - 1];
+      int kn = 0;
+      for (int g = 0; g < Gi; ++g) {
+        int sz = sizes[(d - 1) * Gi + g];
+        if (g == gn) kn = k;
+        if (sz > 0) {
+          LevelInfo li;
+          li.off = (uint16_t)(base + start);
+          li.size = (uint8_t)sz;
+          li.tail_next = 0;
+          li.g = (uint8_t)g;
+          li.pad[0] = li.pad[1] = li.pad[2] = 0;
+          row[k++] = li;
+        }
+        start += sz + 1;
       }
-      start += sz + 1;
+      ncls_d[d - 1] = (uint8_t)k;
+      int tail = 0;
+      for (int q = k - 1; q >= 0; --q) { row[q].tail_next = (uint8_t)tail; tail += row[q].size; }
+      row[0].pad[0] = (uint8_t)kn;
     }
-    ncls_d[d - 1] = (uint8_t)k;
-    int tail = 0;
-    for (int q = k - 1; q >= 0; --q) { row[q].tail_next = (uint8_t)tail; tail += row[q].size; }
-    row[0].pad[0] = (uint8_t)kn;
   }
   if constexpr (ALGO == 1) {
     // the literal walk reads every width's tables; the leaf-parallel search
