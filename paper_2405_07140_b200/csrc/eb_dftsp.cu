@@ -1721,7 +1721,13 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       if (i < n) {
         bool ok = false;
 #pragma unroll
-        for (int q = 0; q < A.prm.ladder_len; ++q) ok |= A.prm.ladder[q] == len_i[h];
+        if constexpr (FK > 0) {
+          // the compiled-in class bound is the ladder length bound (G = ladder_len)
+#pragma unroll
+          for (int q = 0; q < FK % 100; ++q) ok |= (q < A.prm.ladder_len) && A.prm.ladder[q] == len_i[h];
+        } else {
+          for (int q = 0; q < A.prm.ladder_len; ++q) ok |= A.prm.ladder[q] == len_i[h];
+        }
         if (!ok && t_i[h] < bad_t) { bad_t = t_i[h]; bad_i = i; }
       }
     }
@@ -1748,8 +1754,30 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
       int g = 0, kr = 0;
       if constexpr (NI == 1) {
         // class index: class leaders with a shorter output; rank among peers
-        for (unsigned fm = fmask[0]; fm; fm &= fm - 1) g += a_len[__ffs(fm) - 1] < len_i[h];
-        for (unsigned pm = peers & ~(1u << lane); pm; pm &= pm - 1) kr += (int)(a_key[__ffs(pm) - 1] < key_i[h]);
+        if constexpr (FK > 0) {
+          // at most FK % 100 class leaders
+          unsigned fm = fmask[0];
+#pragma unroll
+          for (int q = 0; q < FK % 100; ++q) {
+            if (fm) { g += a_len[__ffs(fm) - 1] < len_i[h]; fm &= fm - 1; }
+          }
+        } else {
+          for (unsigned fm = fmask[0]; fm; fm &= fm - 1) g += a_len[__ffs(fm) - 1] < len_i[h];
+        }
+        // within-class key rank: two peers per step (independent chains)
+        unsigned pm = peers & ~(1u << lane);
+        int kr2 = 0;
+        while (pm) {
+          const int j0 = __ffs(pm) - 1;
+          pm &= pm - 1;
+          kr += (int)(a_key[j0] < key_i[h]);
+          if (pm) {
+            const int j1 = __ffs(pm) - 1;
+            pm &= pm - 1;
+            kr2 += (int)(a_key[j1] < key_i[h]);
+          }
+        }
+        kr += kr2;
         for (unsigned pm = peers & key_ties; pm; pm &= pm - 1) kr += (int)(a_id[__ffs(pm) - 1] < id_i[h]);
       } else {
         // class index: leaders with a shorter output (kr came with the ranks)
