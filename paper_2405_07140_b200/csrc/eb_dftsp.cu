@@ -67,6 +67,7 @@ struct Lay {
   size_t ring_v, ring_p, ring_done, sol;
   size_t pq, pre, pf;                                       // v2: unranking / call prefix / F tables
   size_t pm;                                                // v2, K <= 64: class-list positions per width
+  size_t c_kd;                                              // v2, K <= 64: (k_up s, k_dn n) per class-list position
   size_t total;
   int T;
 };
@@ -110,8 +111,9 @@ __host__ __device__ constexpr inline Lay make_lay(int K, int G, bool exact, bool
     L.pf = L.pq;
     L.pre = take(4 * 64 + 8 * 32);
     L.pm = K <= 64 ? take(8 * (size_t)K) : 0;
+    if (K <= 64) { o = (o + 15) & ~size_t(15); L.c_kd = take(16 * (size_t)K); } else { L.c_kd = 0; }
   } else {
-    L.pq = L.pre = L.pf = L.pm = 0;
+    L.pq = L.pre = L.pf = L.pm = L.c_kd = 0;
   }
   L.total = (o + 15) & ~size_t(15);   // 16-byte warp stride: a_tau (offset 0) is read as double2
   return L;
@@ -443,6 +445,7 @@ struct CountsMode {
   const uint8_t* c_list;
   const double* o_key;      // k_up * s  per tau rank
   const double* o_dnt;      // k_down * n per tau rank
+  const double2* c_kd;      // (k_up * s, k_down * n) per class-list position (K <= 64)
 };
 
 // SearchTables.build (dftsp.py:110-132) for class g of pool width d: the
@@ -1007,11 +1010,12 @@ __device__ bool search_v2(int& passed, int n, int Gi, unsigned char* smem, const
             // the width mask from the class start on
             WMask bits = (WMask)pm[dd - 1] & ((WMask)~(WMask)0 << cm.c_start[li.g]);
             for (int q = 0; q < cc; ++q) {
-              const int t = cm.c_list[wm_ffs(bits)];
+              const int p = wm_ffs(bits);
               bits &= bits - 1;
-              cu = add(cu, cm.o_key[t]);
-              cdn = add(cdn, cm.o_dnt[t]);
-              if (EXACT) tm = pymin(tm, o_tau[t]);
+              const double2 kd = cm.c_kd[p];                    // no tau-rank indirection
+              cu = add(cu, kd.x);
+              cdn = add(cdn, kd.y);
+              if (EXACT) tm = pymin(tm, o_tau[cm.c_list[p]]);
             }
           } else {
             for (int p = cm.c_start[li.g], taken = 0; taken < cc; ++p) {
@@ -1824,7 +1828,11 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
 #pragma unroll
   for (int h = 0; h < NI; ++h) {
     int i = lane + 32 * h;
-    if (i < n) c_list[c_start[gcls_i[h]] + kr_i[h]] = (uint8_t)t_i[h];
+    if (i < n) {
+      const int p = c_start[gcls_i[h]] + kr_i[h];
+      c_list[p] = (uint8_t)t_i[h];
+      if constexpr (ALGO == 2 && NI <= 2) ((double2*)(smem + L.c_kd))[p] = make_double2(key_i[h], dnt_i[h]);
+    }
   }
   __syncwarp();
   if constexpr (ALGO == 2 && NI <= 2) {
@@ -1974,7 +1982,8 @@ __device__ void solve_instance(const DftspArgs& A, int64_t inst, unsigned char* 
     if (!search_v2<PRUNE, INCL, EXACT, NI, FK>(passed, n, Gi, smem, L, lvl, ncls_d, c_len, c_w, o_tau, k2, k3,
                                        slot_base, C.has_cap, padded, traj, found, zf, dwin, kwin, W0, W1, best,
                                        tot_v, tot_p,
-                                       CountsMode{A.prm.exhaustive_counts != 0, c_start, c_list, o_key, o_dnt},
+                                       CountsMode{A.prm.exhaustive_counts != 0, c_start, c_list, o_key, o_dnt,
+                                                  ALGO == 2 && NI <= 2 ? (const double2*)(smem + L.c_kd) : nullptr},
                                        A.ctab, sizes)) {
       // leaf counts overflow the u32 unranking tables: hand the instance to
       // the literal walk (second pass of launch_dftsp)
