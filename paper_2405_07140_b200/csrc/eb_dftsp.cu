@@ -2343,7 +2343,7 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   __shared__ int s_q[3];           // round bases, two rounds ahead (ring of 3)
   __shared__ DCtx s_dc[EB_DC_CACHE];   // derived constants of the first contexts
-  __shared__ DCtx s_dw[16];            // per warp: a context past the cache
+  __shared__ DCtx s_dw[16];            // per warp: a context past the cache (<= 16 warps per block)
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   constexpr size_t WB = al8(make_lay(FK > 0 ? FK / 100 : 1, FK > 0 ? FK % 100 : 1, EXACT, true).total);
   unsigned char* smem = smem_all + warp * (FK > 0 ? WB : A.warp_bytes);
@@ -2386,8 +2386,20 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
   }
 }
 
+// The config-2 shape (FK = 3203) runs at 80 registers and 24 warps per SM:
+// 211 M against 184 M inst/s at 128 registers and 16 warps (spills are 132 B
+// per thread, L1-resident); config 5 (2005) measured the opposite (83 M at 80
+// registers against 97 M), so the other variants keep 128.
+#ifndef EB_LOCK3203_THREADS
+#define EB_LOCK3203_THREADS 256
+#endif
+#ifndef EB_LOCK3203_MINB
+#define EB_LOCK3203_MINB 3
+#endif
 template <bool PRUNE, bool INCL, bool EXACT, int NI, int FK = 0>
-__global__ void __launch_bounds__(EB_LOCK_THREADS, EB_LOCK_MINB) dftsp_lock_kernel(const __grid_constant__ DftspArgs A) {
+__global__ void __launch_bounds__(FK == 3203 ? EB_LOCK3203_THREADS : EB_LOCK_THREADS,
+                                  FK == 3203 ? EB_LOCK3203_MINB : EB_LOCK_MINB)
+    dftsp_lock_kernel(const __grid_constant__ DftspArgs A) {
   lock_loop<PRUNE, INCL, EXACT, NI, FK>(A);
 }
 
