@@ -2396,9 +2396,23 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
 #ifndef EB_LOCK3203_MINB
 #define EB_LOCK3203_MINB 3
 #endif
+#ifndef EB_LOCK2005_THREADS
+#define EB_LOCK2005_THREADS EB_LOCK_THREADS
+#endif
+#ifndef EB_LOCK2005_MINB
+#define EB_LOCK2005_MINB EB_LOCK_MINB
+#endif
+#ifndef EB_LOCK6403_THREADS
+#define EB_LOCK6403_THREADS EB_LOCK_THREADS
+#endif
+#ifndef EB_LOCK6403_MINB
+#define EB_LOCK6403_MINB EB_LOCK_MINB
+#endif
 template <bool PRUNE, bool INCL, bool EXACT, int NI, int FK = 0>
-__global__ void __launch_bounds__(FK == 3203 ? EB_LOCK3203_THREADS : EB_LOCK_THREADS,
-                                  FK == 3203 ? EB_LOCK3203_MINB : EB_LOCK_MINB)
+__global__ void __launch_bounds__(FK == 3203 ? EB_LOCK3203_THREADS : FK == 2005 ? EB_LOCK2005_THREADS
+                                  : FK == 6403 ? EB_LOCK6403_THREADS : EB_LOCK_THREADS,
+                                  FK == 3203 ? EB_LOCK3203_MINB : FK == 2005 ? EB_LOCK2005_MINB
+                                  : FK == 6403 ? EB_LOCK6403_MINB : EB_LOCK_MINB)
     dftsp_lock_kernel(const __grid_constant__ DftspArgs A) {
   lock_loop<PRUNE, INCL, EXACT, NI, FK>(A);
 }
@@ -2721,6 +2735,7 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
     else if (fk == 6403) { EB_PICKLP(2, 6403) }
     else if (K <= 32) { EB_PICKL3(1, 0) } else { EB_PICKL3(2, 0) }
 #undef EB_PICKLP
+
     {
       struct WCache { void (*k)(DftspArgs); size_t wb; int cap; int dev; int w; };
       static thread_local WCache wc[8];
@@ -2734,7 +2749,10 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
       if (best_w < 0) {
         int best_res = 0;
         best_w = 1;
-        for (int w = 1; w <= cap_w; ++w) {
+        cudaFuncAttributes fa;                 // never wider than the launch bounds allow
+        EB_CUDA(cudaFuncGetAttributes(&fa, kern));
+        const int wlim = cap_w < fa.maxThreadsPerBlock / 32 ? cap_w : fa.maxThreadsPerBlock / 32;
+        for (int w = 1; w <= wlim; ++w) {
           const size_t sm = A.warp_bytes * w;
           if (sm > smem_cap) break;
           if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
