@@ -45,12 +45,41 @@ __device__ __forceinline__ uint64_t binom(int n, int k) {
   return g_binom[n][k];
 }
 
+// Binomials C(m, k) for m, k <= nmax, copied into shared memory per block
+// (the scan reads one per step and nmax + z per unranking; global g_binom
+// reads were ~12% of the range kernel's stall samples, r02 ncu capture).
+struct Binom {
+  const uint64_t* t;
+  int s;               // row stride (nmax + 1)
+  __device__ __forceinline__ uint64_t operator()(int n, int k) const {
+    if (k < 0 || n < 0 || k > n) return 0;
+    return t[n * s + k];
+  }
+};
+__device__ Binom binom_smem(uint64_t* dst, int nmax) {
+  const int s = nmax + 1;
+  for (int e = threadIdx.x; e < s * s; e += blockDim.x) dst[e] = g_binom[e / s][e % s];
+  return Binom{dst, s};
+}
+// Per-thread combination idx[0..z) in shared memory, one byte per position,
+// positions strided by the block width (no local-memory stack).
+struct Idx {
+  uint8_t* p;
+  int s;
+  __device__ __forceinline__ uint8_t& operator[](int j) const { return p[j * s]; }
+};
+// dynamic shared memory of the scanning kernels: binomial table, then idx
+__host__ __device__ inline size_t scan_smem_bytes(int nmax, int threads) {
+  return (size_t)(nmax + 1) * (nmax + 1) * 8 + (size_t)nmax * threads;
+}
+
 // Per-instance member terms, in pool order (check_direct's summation order).
 struct Members {
   double a[EB_MAX_K];      // float(s) * k_up       feasibility.py:204
   double b[EB_MAX_K];      // float(n) * k_down     feasibility.py:205
   double ws[EB_MAX_K];     // waiting + slots       feasibility.py:222
   double dl[EB_MAX_K];     // deadline
+  double sl[EB_MAX_K];     // slack dl - ws (the scan's least-slack member)
   int64_t far[EB_MAX_K];   // flops_autoregressive(padded, n)
   int32_t nout[EB_MAX_K];
   int n;
@@ -194,6 +223,7 @@ __device__ void load_members(Members& S, const Ctx& c, const eb_requests& req, i
     S.b[i] = mul(i2d(no), kd);
     S.ws[i] = add(req.waiting_s[r], c.slots);
     S.dl[i] = req.deadline_s[r];
+    S.sl[i] = sub(S.dl[i], S.ws[i]);
     S.far[i] = flops_autoregressive(c.m, padded, no);
     S.nout[i] = no;
   }
@@ -212,7 +242,7 @@ __device__ void load_members(Members& S, const Ctx& c, const eb_requests& req, i
 }
 
 // check_direct on the current combination given its prefix folds.
-__device__ __forceinline__ bool feasible(const Members& S, int z, const uint8_t* idx,
+__device__ __forceinline__ bool feasible(const Members& S, int z, const Idx& idx, int tight, int last,
                                          double up, double dn, int64_t sn, int64_t sf) {
   if (!(leq(up, 1.0) && leq(dn, 1.0))) return false;
   int64_t mem = S.m1 + S.kvp * z;
@@ -221,6 +251,9 @@ __device__ __forceinline__ bool feasible(const Members& S, int z, const uint8_t*
   int64_t flops = (int64_t)z * S.fi + sf;
   double cs = div(mul(S.beta, i2d(flops)), S.C);
   if (S.has_cap && !leq(cs, S.cap_s)) return false;
+  // every member must meet its deadline (an AND, so the order is free): the
+  // prefix member with the least slack and the last member first, then all
+  if (!leq(add(S.ws[tight], cs), S.dl[tight]) || !leq(add(S.ws[last], cs), S.dl[last])) return false;
   for (int j = 0; j < z; ++j)
     if (!leq(add(S.ws[idx[j]], cs), S.dl[idx[j]])) return false;
   return true;
@@ -270,10 +303,9 @@ struct ScanCounters {
   unsigned long long pruned;    // prefixes cut by prefix_infeasible (whole subtrees skipped)
 };
 
-__device__ int64_t scan_chunk(const Members& S, int z, int64_t r_lo, int64_t r_hi,
-                              const unsigned long long* stop, ScanCounters& cnt) {
+__device__ int64_t scan_chunk(const Members& S, const Binom& binom, const Idx& idx, int z, int64_t r_lo,
+                              int64_t r_hi, const unsigned long long* stop, ScanCounters& cnt) {
   const int n = S.n;
-  uint8_t idx[EB_MAX_K];
   {
     uint64_t r = (uint64_t)r_lo;
     int v = 0;
@@ -300,13 +332,15 @@ __device__ int64_t scan_chunk(const Members& S, int z, int64_t r_lo, int64_t r_h
       double pu = 0.0, pd = 0.0;
       int64_t ps = 0, pf = 0;
       int t = idx[0];
+      double tsl = S.sl[t];
       for (int j = 0; j < z - 1; ++j) {
         const int i = idx[j];
         pu = add(pu, S.a[i]);
         pd = add(pd, S.b[i]);
         ps += S.nout[i];
         pf += S.far[i];
-        if (j > 0 && !(sub(S.dl[t], S.ws[t]) <= sub(S.dl[i], S.ws[i]))) t = i;
+        const double sli = S.sl[i];
+        if (j > 0 && !(tsl <= sli)) { t = i; tsl = sli; }
         if (j >= from && !first && prefix_infeasible(S, z, j + 1, pu, pd, ps, pf, t)) {
           q = j;
           dead = true;
@@ -321,8 +355,8 @@ __device__ int64_t scan_chunk(const Members& S, int z, int64_t r_lo, int64_t r_h
     } else {
       const int i = idx[z - 1];
       ++cnt.leaves;
-      (void)ct;
-      if (feasible(S, z, idx, add(cu, S.a[i]), add(cd, S.b[i]), cs + S.nout[i], cf + S.far[i])) return rank;
+      // ct is a prefix member (positions 0..z-2); at z = 1 there is no prefix
+      if (feasible(S, z, idx, z > 1 ? ct : i, i, add(cu, S.a[i]), add(cd, S.b[i]), cs + S.nout[i], cf + S.far[i])) return rank;
     }
     first = false;
     rank += (int64_t)binom(n - idx[q] - 1, z - q - 1);
@@ -382,6 +416,10 @@ __global__ void __launch_bounds__(256) exh_batch_kernel(const __grid_constant__ 
   __shared__ Members S;
   __shared__ unsigned long long best;
   __shared__ unsigned long long next;
+  extern __shared__ __align__(8) unsigned char dyn[];
+  const int nmax = A.cap < 1 ? 1 : A.cap < EB_MAX_K ? A.cap : EB_MAX_K;
+  const Binom bt = binom_smem((uint64_t*)dyn, nmax);
+  const Idx idx{dyn + (size_t)(nmax + 1) * (nmax + 1) * 8 + threadIdx.x, (int)blockDim.x};
   ScanCounters cnt{0ULL, 0ULL};
   for (int64_t inst = blockIdx.x; inst < A.n_inst; inst += gridDim.x) {
     int64_t row0 = A.offsets[inst];
@@ -423,7 +461,7 @@ __global__ void __launch_bounds__(256) exh_batch_kernel(const __grid_constant__ 
         const uint64_t lo = atomicAdd(&next, per);
         if (lo >= total || lo > *(volatile unsigned long long*)&best) break;
         const uint64_t hi = lo + per < total ? lo + per : total;
-        int64_t r = scan_chunk(S, z, (int64_t)lo, (int64_t)hi, &best, cnt);
+        int64_t r = scan_chunk(S, bt, idx, z, (int64_t)lo, (int64_t)hi, &best, cnt);
         if (r >= 0) { atomicMin(&best, (unsigned long long)r); break; }
       }
       __syncthreads();
@@ -458,6 +496,9 @@ struct RangeArgs {
 // threads take in rank order from a global counter.
 __global__ void __launch_bounds__(256) exh_range_kernel(const __grid_constant__ RangeArgs A) {
   __shared__ Members S;
+  extern __shared__ __align__(8) unsigned char dyn[];
+  const Binom bt = binom_smem((uint64_t*)dyn, A.n);     // visible after load_members' barriers
+  const Idx idx{dyn + (size_t)(A.n + 1) * (A.n + 1) * 8 + threadIdx.x, (int)blockDim.x};
   load_members(S, A.c, A.req, 0, A.n);
   if (S.status) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *A.status = S.status;
@@ -472,7 +513,7 @@ __global__ void __launch_bounds__(256) exh_range_kernel(const __grid_constant__ 
     const int64_t lo = A.lo + (int64_t)off;
     if ((unsigned long long)lo > *(volatile unsigned long long*)A.best) break;
     const int64_t hi = lo + A.per < A.hi ? lo + A.per : A.hi;
-    int64_t r = scan_chunk(S, A.z, lo, hi, A.best, cnt);
+    int64_t r = scan_chunk(S, bt, idx, A.z, lo, hi, A.best, cnt);
     if (r >= 0) { atomicMin(A.best, (unsigned long long)r); break; }
   }
   flush_counters(cnt, A.stats);
@@ -508,7 +549,10 @@ int launch_exh_batch(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, in
   BatchArgs A{d_ctxs, n_ctx, n_inst, d_off, d_ci, req_base, d_req, cap, d_status, d_z, d_rank, d_nodes, d_mask,
               exh_stats(h)};
   int64_t grid = n_inst < (int64_t)h->num_sms * 8 ? n_inst : (int64_t)h->num_sms * 8;
-  exh_batch_kernel<<<(unsigned)grid, 256, 0, st>>>(A);
+  const int nmax = cap < 1 ? 1 : cap < EB_MAX_K ? cap : EB_MAX_K;
+  const size_t dsm = scan_smem_bytes(nmax, 256);
+  if (dsm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(exh_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  exh_batch_kernel<<<(unsigned)grid, 256, dsm, st>>>(A);
   EB_CUDA(cudaGetLastError());
   h->launches += 1;
   return EB_OK;
@@ -567,7 +611,9 @@ int exh_range(eb_handle* h, cudaStream_t st, const eb_context& ctx_host, const e
   int zero = 0;
   EB_CUDA(cudaMemcpyAsync(d_best, init, sizeof(init), cudaMemcpyHostToDevice, st));
   EB_CUDA(cudaMemcpyAsync(d_status, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
-  exh_range_kernel<<<(unsigned)grid, threads, 0, st>>>(A);
+  const size_t dsm = scan_smem_bytes(n, threads);
+  if (dsm > 48 * 1024) EB_CUDA(cudaFuncSetAttribute(exh_range_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  exh_range_kernel<<<(unsigned)grid, threads, dsm, st>>>(A);
   EB_CUDA(cudaGetLastError());
   h->launches += 1;
   unsigned long long b;
