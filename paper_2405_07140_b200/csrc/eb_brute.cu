@@ -104,7 +104,7 @@ struct Members {
 // true only if leq(a, b) is false for every a >= a_lo (leq is monotone in a);
 // the margin (1e-5 of the 1e-9 slack) dwarfs any rounding of the bounds.
 __device__ __forceinline__ bool fails_margin(double a_lo, double b) {
-  const double m = fmax(fmax(1.0, fabs_(a_lo)), fabs_(b));
+  const double m = leq_scale(a_lo, b);
   return sub(a_lo, b) > mul(1.00001e-9, m);
 }
 

@@ -322,7 +322,7 @@ __device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
 
 __device__ __forceinline__ bool fails_with_margin(double a_lo, double b) {
   // true only if leq(a, b) is false for every a >= a_lo (leq is monotone in a)
-  const double m = fmax(fmax(1.0, fabs_(a_lo)), fabs_(b));
+  const double m = leq_scale(a_lo, b);
   return sub(a_lo, b) > mul(1.00001e-9, m);
 }
 

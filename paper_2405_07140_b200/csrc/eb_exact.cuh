@@ -99,12 +99,25 @@ EB_HD double fabs_(double x) { return as_f64(as_u64(x) & 0x7fffffffffffffffULL);
 EB_HD double pymin(double a, double b) { return (b < a) ? b : a; }
 EB_HD double pymax(double a, double b) { return (b > a) ? b : a; }
 
+// max(1.0, abs(a), abs(b)) for leq and its margin variants, on the bit
+// patterns: sign-cleared non-NaN doubles order like their (hi, lo) words, so
+// two 32-bit compares per operand replace three FP64 max sequences (each a
+// DSETP.MAX plus NaN fix-ups on sm_100a).  With a NaN operand the result may
+// differ from Python's max, but then a - b is NaN and every comparison
+// against the scale is false either way, so leq's value is unchanged.
+EB_HD double leq_scale(double a, double b) {
+  const uint64_t ua = as_u64(a), ub = as_u64(b);
+  const uint32_t ha = (uint32_t)(ua >> 32) & 0x7fffffffu, hb = (uint32_t)(ub >> 32) & 0x7fffffffu;
+  const uint32_t la = (uint32_t)ua, lb = (uint32_t)ub;
+  uint32_t hm = 0x3ff00000u, lm = 0u;                 // 1.0
+  if (ha >= 0x3ff00000u) { hm = ha; lm = la; }        // |a| >= 1.0
+  if (hb > hm || (hb == hm && lb > lm)) { hm = hb; lm = lb; }
+  return as_f64(((uint64_t)hm << 32) | lm);
+}
+
 // feasibility.py:28-30  leq(a, b) = a - b <= 1e-9 * max(1.0, abs(a), abs(b))
-// (fmax drops a NaN operand exactly as the comparison chain of Python's max
-// keeps its current value, so m is the same double.)
 EB_HD bool leq(double a, double b) {
-  const double m = fmax(fmax(1.0, fabs_(a)), fabs_(b));
-  return sub(a, b) <= mul(1e-9, m);
+  return sub(a, b) <= mul(1e-9, leq_scale(a, b));
 }
 
 // ---------------------------------------------------------------------------
