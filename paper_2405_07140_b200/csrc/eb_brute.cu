@@ -86,6 +86,7 @@ struct Members {
   int status;              // link-math error (raised inside check_direct)
   int64_t m1, kvp, kv, fi; // weight bytes, kv*padded, kv, flops_initial(padded)
   double alpha, M, beta, C, cap_s;
+  double invC;             // 1/C: the scan's division-free compute-time estimate (cs_est)
   int has_cap;
   // level bounds: sums of the z smallest per-member terms (index z)
   int64_t lo_far[EB_MAX_K + 1];
@@ -234,11 +235,24 @@ __device__ void load_members(Members& S, const Ctx& c, const eb_requests& req, i
     S.kvp = S.kv * (int64_t)padded;
     S.fi = flops_initial(c.m, padded);
     S.alpha = c.alpha; S.M = c.M; S.beta = c.beta; S.C = c.C; S.cap_s = c.cap_s;
+    S.invC = div(1.0, c.C);
     S.has_cap = c.has_cap;
   }
   __syncthreads();
   if (threadIdx.x == 0) S.status = (s_err == INT_MAX) ? 0 : (s_err & 63);
   build_level_bounds(S);
+}
+
+// compute_s = (beta * float(flops)) / C without the division: within ~4 ulp
+// of the exact quotient, so only fails_margin tests (1e-14 relative slack)
+// may read it, and only where the tested value is at least the estimate (the
+// slot cap; a deadline with a non-negative ws) so the error stays below the
+// slack -- a refutation by it is then a refutation of the exact value.
+__device__ __forceinline__ double cs_est(const Members& S, int64_t flops) {
+  return mul(mul(S.beta, i2d(flops)), S.invC);
+}
+__device__ __forceinline__ bool late_est(const Members& S, int t, double ce) {
+  return S.ws[t] >= 0.0 && fails_margin(add(S.ws[t], ce), S.dl[t]);
 }
 
 // check_direct on the current combination given its prefix folds.
@@ -249,6 +263,13 @@ __device__ __forceinline__ bool feasible(const Members& S, int z, const Idx& idx
   mem += S.kv * sn;
   if (!leq(mul(S.alpha, i2d(mem)), S.M)) return false;
   int64_t flops = (int64_t)z * S.fi + sf;
+  {
+    // division-free refutation first (most leaves that reach here fail a
+    // deadline or the slot cap by far more than the estimate's error)
+    const double ce = cs_est(S, flops);
+    if (S.has_cap && fails_margin(ce, S.cap_s)) return false;
+    if (late_est(S, tight, ce) || late_est(S, last, ce)) return false;
+  }
   double cs = div(mul(S.beta, i2d(flops)), S.C);
   if (S.has_cap && !leq(cs, S.cap_s)) return false;
   // every member must meet its deadline (an AND, so the order is free): the
@@ -279,9 +300,9 @@ __device__ __forceinline__ bool prefix_infeasible(const Members& S, int z, int p
     return true;
   const int64_t mem = S.m1 + S.kvp * z + S.kv * (ps + S.lo_n[c]);
   if (!leq(mul(S.alpha, i2d(mem)), S.M)) return true;
-  const double cs = div(mul(S.beta, i2d((int64_t)z * S.fi + pf + S.lo_far[c])), S.C);
-  if (S.has_cap && !leq(cs, S.cap_s)) return true;
-  return !leq(add(S.ws[tight], cs), S.dl[tight]);
+  const double cs = cs_est(S, (int64_t)z * S.fi + pf + S.lo_far[c]);
+  if (S.has_cap && fails_margin(cs, S.cap_s)) return true;
+  return late_est(S, tight, cs);
 }
 
 // Scan ranks [r_lo, r_hi) of level z (lex order) and return the first
