@@ -2390,6 +2390,12 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
 // 211 M against 184 M inst/s at 128 registers and 16 warps (spills are 132 B
 // per thread, L1-resident); config 5 (2005) measured the opposite (83 M at 80
 // registers against 97 M), so the other variants keep 128.
+// Config 2's shape (K <= 20, three classes, default flags) with its own
+// compiled-in layout: 4.8 instead of 6.5 KB of shared memory per warp, which
+// leaves the L1 more room for the 80-register build's spills.
+#ifndef EB_FK2003
+#define EB_FK2003 1
+#endif
 #ifndef EB_LOCK3203_THREADS
 #define EB_LOCK3203_THREADS 256
 #endif
@@ -2409,9 +2415,9 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
 #define EB_LOCK6403_MINB EB_LOCK_MINB
 #endif
 template <bool PRUNE, bool INCL, bool EXACT, int NI, int FK = 0>
-__global__ void __launch_bounds__(FK == 3203 ? EB_LOCK3203_THREADS : FK == 2005 ? EB_LOCK2005_THREADS
+__global__ void __launch_bounds__((FK == 3203 || FK == 2003) ? EB_LOCK3203_THREADS : FK == 2005 ? EB_LOCK2005_THREADS
                                   : FK == 6403 ? EB_LOCK6403_THREADS : EB_LOCK_THREADS,
-                                  FK == 3203 ? EB_LOCK3203_MINB : FK == 2005 ? EB_LOCK2005_MINB
+                                  (FK == 3203 || FK == 2003) ? EB_LOCK3203_MINB : FK == 2005 ? EB_LOCK2005_MINB
                                   : FK == 6403 ? EB_LOCK6403_MINB : EB_LOCK_MINB)
     dftsp_lock_kernel(const __grid_constant__ DftspArgs A) {
   lock_loop<PRUNE, INCL, EXACT, NI, FK>(A);
@@ -2689,7 +2695,8 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
   const bool P = prm.pruning != 0, I = prm.inclusive_bound != 0;
   int fk = 0;
   if (algo == 2) {
-    if (K <= 32 && G <= 3) fk = 3203;
+    if (EB_FK2003 && P && !I && !exact && K <= 20 && G <= 3) fk = 2003;
+    else if (K <= 32 && G <= 3) fk = 3203;
     else if (P && K <= 20 && G <= 5) fk = 2005;
     else if (P && K <= 64 && G <= 3) fk = 6403;
   }
@@ -2730,7 +2737,8 @@ int launch_dftsp(eb_handle* h, cudaStream_t st, const eb_context* d_ctxs, int n_
 #define EB_PICKLP(NI, FK)                                                                              \
   kern = I ? (exact ? dftsp_lock_kernel<true, true, true, NI, FK> : dftsp_lock_kernel<true, true, false, NI, FK>)    \
            : (exact ? dftsp_lock_kernel<true, false, true, NI, FK> : dftsp_lock_kernel<true, false, false, NI, FK>);
-    if (fk == 3203) { EB_PICKL3(1, 3203) }
+    if (fk == 2003) { kern = dftsp_lock_kernel<true, false, false, 1, 2003>; }
+    else if (fk == 3203) { EB_PICKL3(1, 3203) }
     else if (fk == 2005) { EB_PICKLP(1, 2005) }
     else if (fk == 6403) { EB_PICKLP(2, 6403) }
     else if (K <= 32) { EB_PICKL3(1, 0) } else { EB_PICKL3(2, 0) }
