@@ -2343,7 +2343,10 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   __shared__ int s_q[3];           // round bases, two rounds ahead (ring of 3)
   __shared__ DCtx s_dc[EB_DC_CACHE];   // derived constants of the first contexts
-  __shared__ DCtx s_dw[16];            // per warp: a context past the cache (<= 16 warps per block)
+  // per warp: a context past the cache (<= 16 warps per block; the config-2
+  // shapes launch at most 8, and the 2.5 KB saved lets three config-2 blocks
+  // fit the 132 KB shared-memory carveout, leaving 124 KB of L1)
+  __shared__ DCtx s_dw[(FK == 2003 || FK == 3203) ? 8 : 16];
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   constexpr size_t WB = al8(make_lay(FK > 0 ? FK / 100 : 1, FK > 0 ? FK % 100 : 1, EXACT, true).total);
   unsigned char* smem = smem_all + warp * (FK > 0 ? WB : A.warp_bytes);
@@ -2399,6 +2402,7 @@ __device__ __forceinline__ void lock_loop(const DftspArgs& A) {
 #ifndef EB_LOCK3203_THREADS
 #define EB_LOCK3203_THREADS 256
 #endif
+static_assert(EB_LOCK3203_THREADS <= 256, "s_dw holds 8 warps for the FK 2003/3203 kernels");
 #ifndef EB_LOCK3203_MINB
 #define EB_LOCK3203_MINB 3
 #endif
