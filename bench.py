@@ -132,7 +132,7 @@ def ranks_info(world, dev):
     return len(set(got)), dist.get_world_size()
 
 
-def _nvml_sampler(idx: int, conn, stop, period: float):
+def _nvml_sampler(idx: int, conn, stop, period: float, ready=None):
     """Child process: (time, sm_mhz, max_mhz, reasons) every `period` s until `stop` is set."""
     rows = []
     try:
@@ -140,6 +140,8 @@ def _nvml_sampler(idx: int, conn, stop, period: float):
         pynvml.nvmlInit()
         hnd = pynvml.nvmlDeviceGetHandleByIndex(idx)
         mx = float(pynvml.nvmlDeviceGetMaxClockInfo(hnd, pynvml.NVML_CLOCK_SM))
+        if ready is not None:
+            ready.set()
         while not stop.is_set():
             try:
                 rows.append((time.time(), float(pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM)), mx,
@@ -149,6 +151,8 @@ def _nvml_sampler(idx: int, conn, stop, period: float):
             time.sleep(period)
     except Exception:
         pass
+    if ready is not None:
+        ready.set()             # NVML unavailable: do not hold the caller
     conn.send(rows)
     conn.close()
 
@@ -180,8 +184,10 @@ class ClockSampler:
         ctx = mp.get_context("spawn")
         self.parent, child = ctx.Pipe(duplex=False)
         self.stop_ev = ctx.Event()
-        self.proc = ctx.Process(target=_nvml_sampler, args=(idx, child, self.stop_ev, 0.002), daemon=True)
+        ready = ctx.Event()
+        self.proc = ctx.Process(target=_nvml_sampler, args=(idx, child, self.stop_ev, 0.002, ready), daemon=True)
         self.proc.start()
+        ready.wait(30)          # sampling before the warm-up starts (short runs: config 4)
         return self
 
     def begin(self):
@@ -631,6 +637,31 @@ def run_config4(args, world, rank, local):
     gpus_active, comm = ranks_info(world, torch.device("cuda", local))
     if rank != 0:
         return 0
+    # parity sample against the literal C scan (oracle/, test-only checker):
+    # the answer's rank is feasible at its level, and the 2^16 ranks before it
+    # are not (tests/test_gpu_brute_large.py checks whole levels)
+    parity = None
+    if not args.no_cpu:
+        import oracle
+        bad, cpu_n, cpu_s = [], 0, 0.0
+        for i, ((rec, cols), o) in enumerate(zip(insts, out[:len(insts)])):
+            z, r = int(o[0]), int(o[1])
+            if z == 0:
+                continue
+            level = oracle.level_evaluator(rec, cols)
+            t1 = time.perf_counter()
+            below = level(z, max(0, r - (1 << 16)), r)
+            cpu_s += time.perf_counter() - t1
+            cpu_n += r - max(0, r - (1 << 16))
+            if level(z, r, r + 1) != r or below != -1:
+                bad.append(i)
+        parity = {"ok": not bad, "instances": len(insts),
+                  "check": "C restatement (oracle/): rank r* feasible at level z*, ranks [r*-2^16, r*) infeasible"}
+        if bad:
+            parity["mismatched"] = bad
+        cpu4 = {"value": round(cpu_n / cpu_s, 1) if cpu_s > 0 else None, "unit": "checked subsets/s", "cores": 1,
+                "kind": "port", "sample": f"{cpu_n} ranks just below each answer (the parity sample), literal "
+                                          "check_direct scan of the C restatement (oracle/), one thread"}
     n_solved = args.steps * len(insts)
     line = {"metric": "brute-force exhaustive_optimal instances/sec (K=%d) and checked subsets/sec" % K,
             "value": round(n_solved / wall, 4), "unit": "instances/s", "n_gpus": world, "steps": args.steps,
@@ -641,10 +672,13 @@ def run_config4(args, world, rank, local):
             "checked_subsets_per_s": round(float(checked[0].item()) / wall, 1),
             "pruned_prefixes_per_s": round(float(checked[1].item()) / wall, 1),
             "reference_nodes_per_s": round(sum(o[2] for o in out[:len(insts)]) * args.steps / wall, 1),
-            "results": [list(o) for o in out[:len(insts)]],
+            "results": [list(o) for o in out[:len(insts)]], "parity": parity,
+            "cpu_baseline": cpu4 if parity is not None else None,
             "gpus_active": gpus_active, "comm_nranks": comm, "clocks": clocks}
+    if parity is not None and not parity["ok"]:
+        line["value"] = None
     print(json.dumps(line), flush=True)
-    return 0
+    return 0 if parity is None or parity["ok"] else 1
 
 
 if __name__ == "__main__":

@@ -15,7 +15,7 @@ run() { local name=$1; shift; local t0=$(date +%s); timeout 900 "$@" > $O/$name.
 
 has bench    && run bench python bench.py
 has c5       && run bench_c5 python bench.py --config 5 --no-cpu
-has c4       && run bench_c4 python bench.py --config 4 --steps 2 --warmup 1
+has c4       && run bench_c4 python bench.py --config 4 --steps 10 --warmup 3
 has ref      && run ref python bench.py --impl reference
 has launches && run launches ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
                     --log-file $O/launches_bench.csv python bench.py --no-cpu
