@@ -83,6 +83,24 @@ def test_branch_and_bound_matches_oracle_many(seed):
         assert (int(st[i]), int(z[i]), int(rk[i]), int(nodes[i]), int(mask[i])) == e, (seed, i)
 
 
+@pytest.mark.parametrize("seed", [31, 32])
+def test_branch_and_bound_raw_negative_waits(seed):
+    """Raw arrays may carry what Request's validation refuses (negative
+    waiting_s, feasibility.py:55-56): the division-free deadline refutations
+    of scan_chunk apply only where ws >= 0, and the answers still equal the
+    oracle's plain enumeration (slot caps and tight deadlines included)."""
+    b, _ = random_batch(seed, 200, k_min=1, k_max=14, slot_cap_frac=0.6)
+    rng = np.random.default_rng(seed)
+    w = b.columns["waiting_s"]
+    neg = rng.random(w.shape[0]) < 0.3
+    w[neg] = -rng.uniform(0.0, 2.0, int(neg.sum())) * b.columns["deadline_s"][neg]
+    st, z, rk, nodes, mask = _run(b)
+    for i in range(b.n_inst):
+        ci = int(b.ctx_index[i])
+        e = oracle.exhaustive(b.contexts[ci:ci + 1], b.columns, int(b.offsets[i]), int(b.offsets[i + 1]))
+        assert (int(st[i]), int(z[i]), int(rk[i]), int(nodes[i]), int(mask[i])) == e, (seed, i)
+
+
 def test_branch_and_bound_config2_pools():
     """Config-2 pools (K=20, BLOOM-3B mix): batch kernel and 5-way rank sharding
     against the oracle's enumeration."""
