@@ -328,14 +328,21 @@ __device__ int64_t scan_chunk(const Members& S, const Binom& binom, const Idx& i
                               int64_t r_hi, const unsigned long long* stop, ScanCounters& cnt) {
   const int n = S.n;
   {
+    // unrank r_lo: position j takes the first v whose block of C(n-v-1,
+    // z-j-1) completions contains r.  r_lo < C(n, z), so every probed row
+    // n-v-1 stays >= z-j-1 >= 0 and the table is read without bounds checks,
+    // walking up one row per step.
     uint64_t r = (uint64_t)r_lo;
     int v = 0;
     for (int j = 0; j < z; ++j) {
+      const uint64_t* p = binom.t + (n - v - 1) * binom.s + (z - j - 1);
       for (;;) {
-        uint64_t c = binom(n - v - 1, z - j - 1);
-        if (r < c) { idx[j] = (uint8_t)v; ++v; break; }
-        r -= c; ++v;
+        const uint64_t c = *p;
+        if (r < c) break;
+        r -= c; ++v; p -= binom.s;
       }
+      idx[j] = (uint8_t)v;
+      ++v;
     }
   }
   double cu = 0.0, cd = 0.0;      // folds of positions 0..z-2 (valid when `cached`)
