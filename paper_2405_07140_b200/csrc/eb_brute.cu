@@ -294,9 +294,11 @@ __device__ __forceinline__ bool feasible(const Members& S, int z, const Idx& idx
 __device__ __forceinline__ bool prefix_infeasible(const Members& S, int z, int p, double pu, double pd,
                                                   int64_t ps, int64_t pf, int tight) {
   const int c = z - p;
-  if (!leq(pu, 1.0) || !leq(pd, 1.0)) return true;
-  if (c > 0 && (fails_margin(mul(add(pu, S.lo_a[c]), 0.999999999999), 1.0) ||
-                fails_margin(mul(add(pd, S.lo_b[c]), 0.999999999999), 1.0)))
+  // uplink / downlink: the prefix sum plus the c smallest remaining terms
+  // (lo_*[0] = 0), refuted with the fails_margin slack (a separate exact
+  // leq of the bare prefix sum only adds refutations inside that slack)
+  if (fails_margin(mul(add(pu, S.lo_a[c]), 0.999999999999), 1.0) ||
+      fails_margin(mul(add(pd, S.lo_b[c]), 0.999999999999), 1.0))
     return true;
   const int64_t mem = S.m1 + S.kvp * z + S.kv * (ps + S.lo_n[c]);
   if (!leq(mul(S.alpha, i2d(mem)), S.M)) return true;
@@ -522,7 +524,12 @@ struct RangeArgs {
 
 // Grid-wide: one level, rank range [lo, hi) in chunks of `per` that the
 // threads take in rank order from a global counter.
-__global__ void __launch_bounds__(256) exh_range_kernel(const __grid_constant__ RangeArgs A) {
+// blocks per SM the range kernel's register budget targets (64 registers and
+// 4 blocks by default; EB_BRUTE_MINB: tuning)
+#ifndef EB_BRUTE_MINB
+#define EB_BRUTE_MINB 1
+#endif
+__global__ void __launch_bounds__(256, EB_BRUTE_MINB) exh_range_kernel(const __grid_constant__ RangeArgs A) {
   __shared__ Members S;
   extern __shared__ __align__(8) unsigned char dyn[];
   const Binom bt = binom_smem((uint64_t*)dyn, A.n);     // visible after load_members' barriers
