@@ -395,8 +395,10 @@ __device__ int64_t scan_chunk(const Members& S, const Binom& binom, const Idx& i
     int j = q;
     while (j >= 0 && idx[j] == n - z + j) --j;
     if (j < 0) break;
-    idx[j] += 1;
-    for (int q2 = j + 1; q2 < z; ++q2) idx[q2] = idx[q2 - 1] + 1;
+    // positions j.. become consecutive from the incremented value: computed
+    // stores, no load-after-store chain through shared memory
+    const int nb = idx[j] + 1 - j;
+    for (int q2 = j; q2 < z; ++q2) idx[q2] = (uint8_t)(nb + q2);
     from = j;
   }
   return -1;
